@@ -1,0 +1,195 @@
+/* hprlp_b200.h -- C ABI of the B200-native HPR-LP iteration loop.
+ *
+ * The reference (/root/reference/pkg/src/hprlp) is pure Python; its only seam on
+ * this path is `solve(problem, cfg) -> SolveReport` (driver.py:281).  The
+ * functions below replace, one for one, the internal steps that `solve` runs
+ * between building ProblemData and writing the report (driver.py:293-372):
+ *
+ *   hpr_analyze      <- SparseMatrix._csr_t (sparse.py:98-100): the explicit
+ *                       transpose, built lazily by the reference on first use
+ *   hpr_scale        <- scale_problem (scaling.py:72-125)
+ *   hpr_power        <- power_method_lambda_max (sparse.py:165-203)
+ *   hpr_run_inner    <- run_inner / iterate_once (core.py:163-179)
+ *   hpr_checkpoint   <- half_step (core.py:118-129) + ScalingInfo.unscale_point
+ *                       (scaling.py:45-49) + clip (driver.py:336) + kkt_residual
+ *                       (driver.py:191-228) + the dot products of m_norm_diff
+ *                       (core.py:182-201) and sigma_update (driver.py:273-274)
+ *   hpr_restart      <- anchor = current = bar (driver.py:363-364)
+ *   hpr_kkt_origin   <- the origin fallback of driver.py:374-380
+ *   hpr_kkt          <- kkt_residual (driver.py:191-228) of a caller-supplied point
+ *   hpr_finalize     <- the final unscale + objectives (driver.py:382-391)
+ *
+ * Conventions
+ *   - Every function returns HPR_OK (0) or a negative HPR_E* code and never
+ *     aborts; hpr_last_error() gives the message of the calling thread's last
+ *     failure.
+ *   - All array pointers are DEVICE pointers owned by the caller (the Python
+ *     host allocates them with PyTorch).  The context owns only its CUDA graphs,
+ *     events, pinned scalar buffers and the carve-up of the caller's workspace.
+ *   - Index arrays are int32 (nnz < 2^31); values are IEEE fp64.
+ *   - Work is asynchronous on the context's stream except where a function
+ *     returns host scalars (hpr_analyze, hpr_scale, hpr_power, hpr_checkpoint,
+ *     hpr_kkt_origin, hpr_finalize), which synchronise once.
+ *   - One context per (device, stream); calls on one context must be serialised
+ *     by the caller; distinct contexts may run concurrently.
+ *   - Non-finite iterates are data (hpr_ckpt_out.nonfinite_k), not errors,
+ *     preserving the reference's status semantics (driver.py:323-326).
+ */
+#ifndef HPRLP_B200_H
+#define HPRLP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPR_OK 0
+#define HPR_EINVAL (-1)
+#define HPR_ECUDA (-2)
+#define HPR_ENCCL (-3)
+#define HPR_ENOMEM (-4)
+#define HPR_ESTATE (-5)
+
+#define HPR_VARIANT_DR 0        /* core.py:146-147 */
+#define HPR_VARIANT_HDR 1       /* core.py:151-153 (HDR and HDR-fixed-sigma) */
+#define HPR_VARIANT_HPR 2       /* core.py:148-150 */
+
+#define HPR_ABI_VERSION 1
+
+typedef struct hpr_ctx hpr_ctx;
+
+typedef struct hpr_dims {
+  int64_t m;    /* rows of the stacked A = [A1; A2] (problem.py:75-82) */
+  int64_t n;    /* columns */
+  int64_t m1;   /* equality rows (first m1 rows) */
+  int64_t nnz;  /* structural nonzeros of the canonical CSR (sparse.py:22-35) */
+} hpr_dims;
+
+/* Device buffers supplied by the caller.  Sizes in element counts. */
+typedef struct hpr_buffers {
+  /* A (m x n), canonical CSR: inputs */
+  const int32_t *a_rp;   /* m+1 */
+  const int32_t *a_ci;   /* nnz, strictly increasing within rows */
+  const double *a_val;   /* nnz, the user's (unscaled) values */
+  double *a_val_s;       /* nnz, scaled values (written by hpr_scale) */
+  /* A^T (n x m), CSR (written by hpr_analyze / hpr_scale) */
+  int32_t *at_rp;        /* n+1 */
+  int32_t *at_ci;        /* nnz */
+  int32_t *at_perm;      /* nnz: A^T entry k is A entry at_perm[k] */
+  double *at_val;        /* nnz, unscaled */
+  double *at_val_s;      /* nnz, scaled */
+  /* original problem vectors: inputs */
+  const double *b, *c, *lower, *upper;      /* m, n, n, n */
+  /* scaled problem and scaling factors (written by hpr_scale) */
+  double *b_s, *c_s, *lower_s, *upper_s;    /* m, n, n, n */
+  double *row_scale, *col_scale;            /* m, n */
+  /* iterate state w = (y, x), anchor, reflection w = 2 xb - x */
+  double *y, *x, *anc_y, *anc_x, *w;        /* m, n, m, n, n */
+  /* checkpoint half-step (scaled space) and scratch */
+  double *yb, *xb, *zb, *dy, *wtmp;         /* m, n, n, m, n */
+  /* candidate (termination-space) points, two slots */
+  double *cand_y[2], *cand_x[2], *cand_z[2];
+} hpr_buffers;
+
+typedef struct hpr_scale_out {
+  double b_factor, c_factor;   /* ScalingInfo.b_norm_factor / c_norm_factor */
+  double bnorm_orig, cnorm_orig, bnorm_s, cnorm_s;  /* ||b||, ||c|| of both problems */
+} hpr_scale_out;
+
+typedef struct hpr_power_out {
+  double value;      /* raw * (1 + 1e-3) (sparse.py:202) */
+  double raw;
+  int32_t iterations;
+  int32_t converged;
+} hpr_power_out;
+
+/* Scalars of one checkpoint.  Sums of squares / dot products are reduced in a
+ * fixed order (deterministic, bit-reproducible run to run). */
+typedef struct hpr_ckpt_out {
+  /* half step, scaled space */
+  double bar_dx2;   /* ||xb - anchor_x||^2          (driver.py:273) */
+  double bar_dy2;   /* ||yb - anchor_y||^2          (driver.py:274) */
+  double dy2;       /* ||y - yb||^2                 (core.py:195,197) */
+  double dx2;       /* ||x - xb||^2                 (core.py:197) */
+  double sh2;       /* ||dx + sigma A^T dy||^2      (core.py:192-193) */
+  double aty2;      /* ||A^T dy||^2                 (core.py:195) */
+  /* KKT on the termination-space problem (driver.py:203-216) */
+  double prim2;     /* ||Pi_D(b - A x)||^2 */
+  double dual2;     /* ||c - A^T y - z||^2 */
+  double r1sq, r2sq;
+  double cx;        /* <c, x> */
+  double by;        /* <b, y> */
+  double lz, uz;    /* sum l_i z_i (z_i > 0, l_i finite), sum u_i z_i (z_i < 0, u_i finite) */
+  int64_t n_lo, n_up, clamped;
+  int64_t nonfinite_k;  /* first iteration k with a non-finite iterate, or -1 */
+} hpr_ckpt_out;
+
+int hpr_abi_version(void);
+const char *hpr_last_error(void);
+
+/* Bytes of the workspace the caller must allocate for these dims. */
+int hpr_workspace_bytes(const hpr_dims *dims, size_t *bytes);
+
+/* stream: a cudaStream_t (non-default) the context works on. */
+int hpr_ctx_create(hpr_ctx **out, const hpr_dims *dims, int device, void *stream);
+int hpr_ctx_destroy(hpr_ctx *ctx);
+
+int hpr_bind(hpr_ctx *ctx, const hpr_buffers *bufs, void *workspace, size_t workspace_bytes);
+
+/* Builds A^T (stable: rows ascending within each column, matching
+ * csr_matrix(A.T)), its permutation and the row tilings of A and A^T. */
+int hpr_analyze(hpr_ctx *ctx);
+
+/* Ruiz(ruiz_iters) -> Pock-Chambolle(alpha=1) -> b/c normalisation on the
+ * device.  With all three off the scaled problem is a copy (identity_scaling). */
+int hpr_scale(hpr_ctx *ctx, int ruiz_iters, int pock_chambolle, int bc_normalize,
+              hpr_scale_out *out);
+
+/* Power method for lambda_1(A A^T) of the scaled A.  *zero_ata set if the
+ * all-ones and every basis start vector have A^T v = 0 (caller raises). */
+int hpr_power(hpr_ctx *ctx, double tol, int max_iters, hpr_power_out *out);
+
+/* y = x = anchors = 0; clears the non-finite marker. */
+int hpr_state_reset(hpr_ctx *ctx);
+
+/* `steps` iterations from inner counter t and total counter k with penalty
+ * sigma and lam*sigma (the reference's single rounded product, core.py:170).
+ * Replays a cached CUDA graph of `steps` iterations.  Asynchronous. */
+int hpr_run_inner(hpr_ctx *ctx, int steps, int64_t t, int64_t k, double sigma,
+                  double lamsig, int variant);
+
+/* Half step + candidate (slot) + KKT + merit/sigma dot products.  One sync. */
+int hpr_checkpoint(hpr_ctx *ctx, double sigma, double lamsig, int term_original, int slot,
+                   hpr_ckpt_out *out);
+
+/* anchor = current = (yb, xb) of the last checkpoint.  Asynchronous. */
+int hpr_restart(hpr_ctx *ctx);
+
+/* Candidate (slot) = (0, 0, clip(0, l, u)) on the termination problem and its KKT. */
+int hpr_kkt_origin(hpr_ctx *ctx, int term_original, int slot, hpr_ckpt_out *out);
+
+/* KKT residual terms of whatever the caller stored in candidate `slot`
+ * (kkt_residual, driver.py:191-228, on the original or the scaled problem). */
+int hpr_kkt(hpr_ctx *ctx, int term_original, int slot, hpr_ckpt_out *out);
+
+/* Final solution: for the scaled termination space, unscale candidate `slot`
+ * into slot `1 - slot` and clip; objectives of the solution on the original
+ * problem are returned in out->cx / by / lz / uz / n_lo / n_up. */
+int hpr_finalize(hpr_ctx *ctx, int term_original, int slot, hpr_ckpt_out *out);
+
+/* Kernel launches issued by this context so far (graph nodes counted per replay). */
+int hpr_launch_count(hpr_ctx *ctx, int64_t *count);
+
+/* Tile statistics of the analysed matrices (for roofline bookkeeping). */
+int hpr_tile_info(hpr_ctx *ctx, int64_t *ntiles_a, int64_t *ntiles_at);
+
+/* Device time (ms) of the last hpr_run_inner and of the last checkpoint,
+ * measured with CUDA events on the context stream. */
+int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPRLP_B200_H */

@@ -1,0 +1,27 @@
+"""B200-native HPR-LP: the restarted Halpern Peaceman-Rachford LP iteration
+loop (arXiv 2408.12179) on hand-written sm_100a CUDA.
+
+Drop-in for the reference's solve path: ``solve(problem, cfg) -> SolveReport``
+with the reference's ``SolverConfig`` option names and ``SolveReport`` result
+object (reference ``hprlp/driver.py``).  The arithmetic runs in
+``libhprlp_b200.so`` (C ABI: ``include/hprlp_b200.h``); there is no CPU path.
+"""
+
+from .driver import (KktResidual, RestartEvent, RestartKind, SolveReport, SolverConfig,
+                     SolveStatus, Timings, Variant, check_restart, check_termination,
+                     kkt_residual, sigma_guards_pass, solve)
+from .generators import generate_flow_lp, generate_known_solution_lp, generate_planted_lp_fast
+from .problem import (DimensionMismatchError, LpProblem, PrimalDualPoint, SparseMatrix,
+                      dual_objective, primal_objective, project_onto_box,
+                      project_onto_dual_cone)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DimensionMismatchError", "KktResidual", "LpProblem", "PrimalDualPoint", "RestartEvent",
+    "RestartKind", "SolveReport", "SolveStatus", "SolverConfig", "SparseMatrix", "Timings",
+    "Variant", "check_restart", "check_termination", "dual_objective",
+    "generate_flow_lp", "generate_known_solution_lp", "generate_planted_lp_fast",
+    "kkt_residual", "primal_objective", "project_onto_box", "project_onto_dual_cone",
+    "sigma_guards_pass", "solve",
+]
