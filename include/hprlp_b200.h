@@ -6,7 +6,9 @@
  * between building ProblemData and writing the report (driver.py:293-372):
  *
  *   hpr_analyze      <- SparseMatrix._csr_t (sparse.py:98-100): the explicit
- *                       transpose, built lazily by the reference on first use
+ *                       transpose, built lazily by the reference on first use;
+ *                       also plans the SELL-32-sigma iteration layout
+ *   hpr_bind_layout  <- (no reference counterpart) binds + fills that layout
  *   hpr_scale        <- scale_problem (scaling.py:72-125)
  *   hpr_power        <- power_method_lambda_max (sparse.py:165-203)
  *   hpr_run_inner    <- run_inner / iterate_once (core.py:163-179)
@@ -29,7 +31,7 @@
  *   - Index arrays are int32 (nnz < 2^31); values are IEEE fp64.
  *   - Work is asynchronous on the context's stream except where a function
  *     returns host scalars (hpr_analyze, hpr_scale, hpr_power, hpr_checkpoint,
- *     hpr_kkt_origin, hpr_finalize), which synchronise once.
+ *     hpr_kkt, hpr_kkt_origin, hpr_finalize), which synchronise once.
  *   - One context per (device, stream); calls on one context must be serialised
  *     by the caller; distinct contexts may run concurrently.
  *   - Non-finite iterates are data (hpr_ckpt_out.nonfinite_k), not errors,
@@ -139,16 +141,24 @@ int hpr_ctx_destroy(hpr_ctx *ctx);
 int hpr_bind(hpr_ctx *ctx, const hpr_buffers *bufs, void *workspace, size_t workspace_bytes);
 
 /* Builds A^T (stable: rows ascending within each column, matching
- * csr_matrix(A.T)), its permutation and the row tilings of A and A^T. */
-int hpr_analyze(hpr_ctx *ctx);
+ * csr_matrix(A.T)) and its permutation, and plans the SELL-32-sigma layout of A
+ * and A^T used by every sparse product: slices of 32 rows (one per lane),
+ * rows sorted by length inside windows of 256, entries column-major inside a
+ * slice, rows longer than 1024 kept in CSR.  *layout_bytes receives the size
+ * of the layout buffer the caller must allocate and pass to hpr_bind_layout. */
+int hpr_analyze(hpr_ctx *ctx, size_t *layout_bytes);
+
+/* Binds the layout buffer and fills it (column indices, CSR->slot map,
+ * unscaled values).  Must follow hpr_analyze. */
+int hpr_bind_layout(hpr_ctx *ctx, void *layout, size_t layout_bytes);
 
 /* Ruiz(ruiz_iters) -> Pock-Chambolle(alpha=1) -> b/c normalisation on the
  * device.  With all three off the scaled problem is a copy (identity_scaling). */
 int hpr_scale(hpr_ctx *ctx, int ruiz_iters, int pock_chambolle, int bc_normalize,
               hpr_scale_out *out);
 
-/* Power method for lambda_1(A A^T) of the scaled A.  *zero_ata set if the
- * all-ones and every basis start vector have A^T v = 0 (caller raises). */
+/* Power method for lambda_1(A A^T) of the scaled A; HPR_EINVAL if the all-ones
+ * and every basis start vector have A^T v = 0. */
 int hpr_power(hpr_ctx *ctx, double tol, int max_iters, hpr_power_out *out);
 
 /* y = x = anchors = 0; clears the non-finite marker. */
@@ -182,8 +192,11 @@ int hpr_finalize(hpr_ctx *ctx, int term_original, int slot, hpr_ckpt_out *out);
 /* Kernel launches issued by this context so far (graph nodes counted per replay). */
 int hpr_launch_count(hpr_ctx *ctx, int64_t *count);
 
-/* Tile statistics of the analysed matrices (for roofline bookkeeping). */
-int hpr_tile_info(hpr_ctx *ctx, int64_t *ntiles_a, int64_t *ntiles_at);
+/* Statistics of the SELL layout (slices, slots incl. padding, long rows). */
+typedef struct hpr_layout_info_t {
+  int64_t slices_a, slices_at, slots_a, slots_at, long_rows_a, long_rows_at;
+} hpr_layout_info_t;
+int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 
 /* Device time (ms) of the last hpr_run_inner and of the last checkpoint,
  * measured with CUDA events on the context stream. */

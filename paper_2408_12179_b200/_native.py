@@ -70,6 +70,11 @@ class HprCkptOut(ctypes.Structure):
         ("nonfinite_k", ctypes.c_int64)]
 
 
+class HprLayoutInfo(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ("slices_a", "slices_at", "slots_a", "slots_at",
+                                               "long_rows_a", "long_rows_at")]
+
+
 # name -> (restype, argtypes); every int-returning function is error-checked
 _SIGS = {
     "hpr_abi_version": (ctypes.c_int, []),
@@ -80,7 +85,8 @@ _SIGS = {
     "hpr_ctx_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "hpr_bind": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprBuffers), ctypes.c_void_p,
                                 ctypes.c_size_t]),
-    "hpr_analyze": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_analyze": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
+    "hpr_bind_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "hpr_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.POINTER(HprScaleOut)]),
     "hpr_power": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
@@ -99,8 +105,7 @@ _SIGS = {
     "hpr_finalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(HprCkptOut)]),
     "hpr_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
-    "hpr_tile_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
-                                     ctypes.POINTER(ctypes.c_int64)]),
+    "hpr_layout_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprLayoutInfo)]),
     "hpr_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
 }

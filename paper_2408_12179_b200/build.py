@@ -18,7 +18,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",                 # every product/sum rounded separately, like numpy/scipy
     "-Xcompiler", "-fPIC", "-shared",
-    "-diag-suppress", "177",
+    "-diag-suppress", "177", "-Xcompiler", "-Wno-deprecated-declarations",
 ]
 
 

@@ -1,11 +1,13 @@
 // hpr_capi.cu -- C ABI (include/hprlp_b200.h) over the sm_100a kernels.
 //
-// Host-side orchestration only: workspace carve-up, the transpose/tiling
-// analysis, the scaling and power-method passes, CUDA-graph capture of the
-// inner loop, the checkpoint sequence and its single device->host readback.
+// Host-side orchestration only: workspace carve-up, the transpose and
+// SELL-32-sigma layout analysis, the scaling and power-method passes, CUDA-graph
+// capture of the inner loop, the checkpoint sequence and its single
+// device->host readback.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -42,10 +44,9 @@ int fail(int code, const std::string &msg) {
       return fail(HPR_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));     \
   } while (0)
 
-constexpr int kBucket = 2048;   // tile nonzero bucket
-constexpr int kLongLen = 1024;  // rows longer than this get their own tile
-constexpr int kCap = kBucket + kLongLen;
-constexpr int kPowBatch = 8;    // power steps per graph replay
+constexpr int kPowBatch = 8;      // power steps per graph replay
+constexpr int kMaxGridPerSm = 8;  // CTAs per SM cap of the SELL kernels (partials sizing)
+constexpr int kSumsqBlocks = 1024;
 
 // result slots of the final reduction (see hpr_ckpt_out)
 enum {
@@ -55,24 +56,30 @@ enum {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int64_t tile_bound(int64_t nrows, int64_t nnz) {
-  int64_t b = nnz / kBucket + nrows / kThreads + 2 * (nnz / kLongLen) + 4;
-  return std::min<int64_t>(b, nrows + 1);
-}
+int64_t windows_of(int64_t nrows) { return (nrows + kWindow - 1) / kWindow; }
+
+// per-matrix plan arrays in the main workspace
+struct PlanOff {
+  size_t slice_row, slice_slots, slice_ptr, long_flag, long_rows, nsel;
+};
 
 struct Layout {
-  size_t tiles_a, tiles_at, flags, pos, keys_out, iota, row_of, cub_tmp, cub_bytes, dvec_m,
-      dvec_n, part, part_count, params, pow, results, fac, total;
+  PlanOff pa, pat;
+  size_t keys_out, iota, row_of, cub_tmp, cub_bytes, dvec_m, dvec_n, part, part_count, params,
+      pow, results, fac, total;
 };
 
 int cub_temp_bytes(const hpr_dims &d, size_t *bytes) {
-  size_t s1 = 0, s2 = 0;
-  int nnz = (int)d.nnz;
-  int nmax = (int)std::max(d.m, d.n);
+  size_t s1 = 0, s2 = 0, s3 = 0;
+  const int nnz = (int)d.nnz;
+  const int nmax = (int)std::max(d.m, d.n);
+  const int smax = (int)(windows_of(nmax) * (kWindow / kSlice) + 1);
   CK(cub::DeviceRadixSort::SortPairs(nullptr, s1, (const int *)nullptr, (int *)nullptr,
                                      (const int *)nullptr, (int *)nullptr, nnz, 0, 32));
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, s2, (const int *)nullptr, (int *)nullptr, nmax));
-  *bytes = std::max(s1, s2);
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, s2, (const int *)nullptr, (int *)nullptr, smax));
+  CK(cub::DeviceSelect::Flagged(nullptr, s3, cub::CountingInputIterator<int>(0),
+                                (const int *)nullptr, (int *)nullptr, (int *)nullptr, nmax));
+  *bytes = std::max(s1, std::max(s2, s3));
   return HPR_OK;
 }
 
@@ -81,32 +88,40 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
-    off = align_up(off + bytes, 256);
+    off = align_up(off + std::max<size_t>(bytes, 16), 256);
     return o;
   };
-  const int64_t nmax = std::max(d.m, d.n);
-  const int64_t tb_a = tile_bound(d.m, d.nnz), tb_at = tile_bound(d.n, d.nnz);
-  L.tiles_a = take(sizeof(int) * (tb_a + 1));
-  L.tiles_at = take(sizeof(int) * (tb_at + 1));
-  L.flags = take(sizeof(int) * (nmax + 1));
-  L.pos = take(sizeof(int) * (nmax + 1));
-  L.keys_out = take(sizeof(int) * std::max<int64_t>(d.nnz, 1));
-  L.iota = take(sizeof(int) * std::max<int64_t>(d.nnz, 1));
-  L.row_of = take(sizeof(int) * std::max<int64_t>(d.nnz, 1));
+  auto plan = [&](int64_t nrows) {
+    PlanOff p;
+    const int64_t nw = windows_of(nrows);
+    const int64_t ns = nw * (kWindow / kSlice);
+    p.slice_row = take(sizeof(int) * nw * kWindow);
+    p.slice_slots = take(sizeof(int) * (ns + 1));
+    p.slice_ptr = take(sizeof(int) * (ns + 1));
+    p.long_flag = take(sizeof(int) * nrows);
+    p.long_rows = take(sizeof(int) * nrows);
+    p.nsel = take(sizeof(int));
+    return p;
+  };
+  L.pa = plan(d.m);
+  L.pat = plan(d.n);
+  L.keys_out = take(sizeof(int) * d.nnz);
+  L.iota = take(sizeof(int) * d.nnz);
+  L.row_of = take(sizeof(int) * d.nnz);
   L.cub_bytes = cub_bytes;
-  L.cub_tmp = take(std::max<size_t>(cub_bytes, 16));
-  L.dvec_m = take(sizeof(double) * std::max<int64_t>(d.m, 1));
-  L.dvec_n = take(sizeof(double) * std::max<int64_t>(d.n, 1));
-  // partials: x_half 2, merit 2, kkt_col 8 per A^T tile; y_half 2, kkt_row 3 per A tile;
-  // plus sum-of-squares passes over max(m, n) with up to 4 * 1024 CTAs
-  L.part_count = (size_t)12 * tb_at + (size_t)5 * tb_a + 4 * 1024 + 3 * std::max(tb_a, tb_at);
+  L.cub_tmp = take(cub_bytes);
+  L.dvec_m = take(sizeof(double) * d.m);
+  L.dvec_n = take(sizeof(double) * d.n);
+  // per-CTA partials of the SELL kernels (<= kMaxGridPerSm CTAs per SM, <= 1024 SMs):
+  // x_half 2, y_half 2, merit 2, kkt_row 3, kkt_col 8, pow_t 1, pow_a 2 (= 20),
+  // plus 4 sum-of-squares passes of up to kSumsqBlocks CTAs
+  L.part_count = (size_t)20 * kMaxGridPerSm * 1024 + 4 * kSumsqBlocks;
   L.part = take(sizeof(double) * L.part_count);
   L.params = take(sizeof(IterParams));
   L.pow = take(sizeof(PowState));
   L.results = take(sizeof(double) * 64);
   L.fac = take(sizeof(double) * 2);
   L.total = off;
-  (void)nmax;
   return L;
 }
 
@@ -117,6 +132,16 @@ int grid_for(int64_t n, int threads = 256, int max_blocks = 148 * 16) {
   return (int)b;
 }
 
+// one matrix in SELL form
+struct Sell {
+  int nrows = 0, nslices = 0, nlong = 0;
+  long long slots = 0;
+  int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *long_flag = nullptr,
+      *long_rows = nullptr, *nsel = nullptr;
+  int *ci = nullptr, *pos = nullptr;
+  double *val_s = nullptr, *val0 = nullptr;
+};
+
 }  // namespace
 
 struct hpr_ctx {
@@ -124,11 +149,11 @@ struct hpr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   hpr_buffers B{};
-  bool bound = false, analyzed = false, scaled = false;
+  bool bound = false, analyzed = false, laid_out = false, scaled = false;
   char *ws = nullptr;
   Layout L{};
-  int *tiles_a = nullptr, *tiles_at = nullptr;
-  int ntiles_a = 0, ntiles_at = 0;
+  Sell sa, sat;
+  int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
   PowState *pow = nullptr;
@@ -141,75 +166,127 @@ struct hpr_ctx {
   bool inner_timed = false, ckpt_timed = false;
   long long launches = 0;
 
-  TileMat mat_a(const double *val) const {
-    return TileMat{B.a_rp, B.a_ci, val, tiles_a, ntiles_a, kCap};
+  SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
+    return SellMat{S.slice_ptr, S.slice_row, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
+                   S.long_rows, S.nslices, S.nlong};
   }
-  TileMat mat_at(const double *val) const {
-    return TileMat{B.at_rp, B.at_ci, val, tiles_at, ntiles_at, kCap};
+  SellMat mat_a(bool scaled) const {
+    return mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
   }
-  static size_t smem() { return sizeof(double) * (size_t)(kCap + (kCap >> 4) + 16); }
+  SellMat mat_at(bool scaled) const {
+    return mat(sat, B.at_rp, B.at_ci, scaled ? B.at_val_s : B.at_val, scaled);
+  }
 };
 
 namespace {
 
-int set_smem_attrs() {
-  static bool done = false;
-  if (done) return HPR_OK;
-  const int bytes = (int)hpr_ctx::smem();
-  CK(cudaFuncSetAttribute(k_x_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_y_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_x_half, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_y_half, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_kkt_row, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_kkt_col, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_merit_col, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_pow_t, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CK(cudaFuncSetAttribute(k_pow_a, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done = true;
+// Launch the SELL kernel for epilogue Epi: grid = min(windows, occupancy x SMs);
+// returns the grid (= partials per quantity).
+template <class Epi>
+int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
+                int *grid_out) {
+  static int occ = 0;
+  if (occ == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<Epi>, kThreads, 0));
+    if (occ < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
+    occ = std::min(occ, kMaxGridPerSm);
+  }
+  const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
+  k_sell<Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
+  CKL();
+  c->launches += 1;
+  if (grid_out) *grid_out = grid;
   return HPR_OK;
 }
 
 // parts layout inside ctx->part (in doubles)
 struct Parts {
-  double *xhalf, *yhalf, *krow, *kcol, *merit, *misc;
+  double *xhalf, *yhalf, *merit, *krow, *kcol, *powt, *powa, *misc;
 };
 Parts parts_of(const hpr_ctx *c) {
+  const size_t g = (size_t)kMaxGridPerSm * 1024;
   Parts p;
-  const size_t ta = std::max(c->ntiles_a, 1), tat = std::max(c->ntiles_at, 1);
   p.xhalf = c->part;
-  p.merit = p.xhalf + 2 * tat;
-  p.kcol = p.merit + 2 * tat;
-  p.yhalf = p.kcol + 8 * tat;
-  p.krow = p.yhalf + 2 * ta;
-  p.misc = p.krow + 3 * ta;
+  p.yhalf = p.xhalf + 2 * g;
+  p.merit = p.yhalf + 2 * g;
+  p.krow = p.merit + 2 * g;
+  p.kcol = p.krow + 3 * g;
+  p.powt = p.kcol + 8 * g;
+  p.powa = p.powt + 1 * g;
+  p.misc = p.powa + 2 * g;
   return p;
 }
 
-// partial buffer for a k_sumsq pass over n elements (<= 1024 CTAs)
-int sumsq_blocks(int64_t n) { return grid_for(n, kThreads, 1024); }
+int sumsq_blocks(int64_t n) { return grid_for(n, kThreads, kSumsqBlocks); }
 
-int build_tiles(hpr_ctx *c, const int *rp, int nrows, int *tile_row, int *ntiles_out) {
-  int *flags = (int *)(c->ws + c->L.flags);
-  int *pos = (int *)(c->ws + c->L.pos);
-  const int g = grid_for(nrows);
-  k_tile_flags<<<g, 256, 0, c->stream>>>(rp, nrows, kBucket, kLongLen, flags);
+// SELL plan of one matrix: slice order, slot offsets, long-row list
+int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) {
+  S.nrows = nrows;
+  const int nw = (int)windows_of(nrows);
+  S.nslices = nw * (kWindow / kSlice);
+  S.slice_row = (int *)(c->ws + po.slice_row);
+  S.slice_slots = (int *)(c->ws + po.slice_slots);
+  S.slice_ptr = (int *)(c->ws + po.slice_ptr);
+  S.long_flag = (int *)(c->ws + po.long_flag);
+  S.long_rows = (int *)(c->ws + po.long_rows);
+  S.nsel = (int *)(c->ws + po.nsel);
+  cudaStream_t s = c->stream;
+  CK(cudaMemsetAsync(S.slice_slots + S.nslices, 0, sizeof(int), s));
+  k_sell_plan<<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_slots, S.long_flag);
   CKL();
   size_t tb = c->L.cub_bytes;
-  CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, flags, pos, nrows, c->stream));
-  k_tile_scatter<<<g, 256, 0, c->stream>>>(flags, pos, nrows, tile_row);
-  CKL();
+  CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, S.slice_slots, S.slice_ptr,
+                                   S.nslices + 1, s));
+  tb = c->L.cub_bytes;
+  CK(cub::DeviceSelect::Flagged(c->ws + c->L.cub_tmp, tb, cub::CountingInputIterator<int>(0),
+                                S.long_flag, S.long_rows, S.nsel, nrows, s));
   c->launches += 3;
-  int hp = 0, hf = 0;
-  CK(cudaMemcpyAsync(&hp, pos + nrows - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(&hf, flags + nrows - 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  *ntiles_out = hp + hf;
+  int total = 0, nl = 0;
+  CK(cudaMemcpyAsync(&total, S.slice_ptr + S.nslices, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&nl, S.nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (total < 0) return fail(HPR_EINVAL, "SELL slot count overflows int32");
+  S.slots = total;
+  S.nlong = nl;
+  return HPR_OK;
+}
+
+size_t sell_bytes(const Sell &S, int64_t nnz) {
+  return align_up((size_t)S.slots * 4 + 256, 256) + 2 * align_up((size_t)S.slots * 8 + 256, 256) +
+         align_up((size_t)nnz * 4 + 256, 256);
+}
+
+int layout_sell(hpr_ctx *c, char *&p, Sell &S, const int *rp, const int *ci, const double *val0) {
+  const long long nnz = c->d.nnz;
+  cudaStream_t s = c->stream;
+  S.ci = (int *)p;
+  p += align_up((size_t)S.slots * 4 + 256, 256);
+  S.val_s = (double *)p;
+  p += align_up((size_t)S.slots * 8 + 256, 256);
+  S.val0 = (double *)p;
+  p += align_up((size_t)S.slots * 8 + 256, 256);
+  S.pos = (int *)p;
+  p += align_up((size_t)nnz * 4 + 256, 256);
+  CK(cudaMemsetAsync(S.ci, 0, (size_t)S.slots * 4, s));
+  CK(cudaMemsetAsync(S.val_s, 0, (size_t)S.slots * 8, s));
+  CK(cudaMemsetAsync(S.val0, 0, (size_t)S.slots * 8, s));
+  CK(cudaMemsetAsync(S.pos, 0xff, (size_t)nnz * 4, s));   // -1: long-row entries
+  k_sell_fill<<<grid_for((int64_t)S.nslices * 32), 256, 0, s>>>(rp, ci, S.slice_ptr, S.slice_row,
+                                                                S.nslices, S.ci, S.pos);
+  CKL();
+  if (nnz > 0) {
+    k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(S.pos, val0, S.val0, nnz);
+    CKL();
+  }
+  c->launches += 2;
   return HPR_OK;
 }
 
 // fixed-order final reduction of a list of partial segments into ctx->results
 int reduce_final(hpr_ctx *c, const std::vector<RedSeg> &segs) {
   RedList L{};
+  if (segs.size() > 24) return fail(HPR_EINVAL, "too many reduction segments");
   L.nseg = (int)segs.size();
   for (size_t i = 0; i < segs.size(); ++i) L.seg[i] = segs[i];
   k_reduce_final<<<L.nseg, kThreads, 0, c->stream>>>(L, c->results);
@@ -225,15 +302,6 @@ int fetch_results(hpr_ctx *c) {
                      c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return HPR_OK;
-}
-
-// sum of squares of a device vector into results[slot] (deterministic)
-int sumsq_into(hpr_ctx *c, const double *a, int64_t n, double *partbuf, int slot) {
-  const int nb = sumsq_blocks(n);
-  k_sumsq<<<nb, kThreads, 0, c->stream>>>(a, n, partbuf);
-  CKL();
-  c->launches += 1;
-  return reduce_final(c, {RedSeg{partbuf, nb, slot}});
 }
 
 void fill_out(const hpr_ctx *c, hpr_ckpt_out *o) {
@@ -258,37 +326,54 @@ void fill_out(const hpr_ctx *c, hpr_ckpt_out *o) {
   o->nonfinite_k = c->h_params->nonfinite_k == ULLONG_MAX ? -1 : (int64_t)c->h_params->nonfinite_k;
 }
 
-// KKT kernels on the termination problem for candidate `slot` (+ reduction segments)
+// KKT kernels on the termination problem for a candidate (+ reduction segments)
 int launch_kkt(hpr_ctx *c, int term_original, const double *cy, const double *cx,
                const double *cz, std::vector<RedSeg> &segs) {
   const hpr_buffers &B = c->B;
   Parts P = parts_of(c);
-  const size_t sm = hpr_ctx::smem();
-  const double *aval = term_original ? B.a_val : B.a_val_s;
-  const double *atval = term_original ? B.at_val : B.at_val_s;
-  k_kkt_row<<<c->ntiles_a, kThreads, sm, c->stream>>>(c->mat_a(aval), cx, cy,
-                                                       term_original ? B.b : B.b_s,
-                                                       (int)c->d.m1, P.krow);
-  CKL();
-  k_kkt_col<<<c->ntiles_at, kThreads, sm, c->stream>>>(
-      c->mat_at(atval), cy, cx, cz, term_original ? B.c : B.c_s,
-      term_original ? B.lower : B.lower_s, term_original ? B.upper : B.upper_s, P.kcol);
-  CKL();
-  c->launches += 2;
-  const int ta = c->ntiles_a, tat = c->ntiles_at;
-  segs.push_back({P.krow + 0 * ta, ta, R_PRIM2});
-  segs.push_back({P.krow + 1 * ta, ta, R_BY});
-  segs.push_back({P.krow + 2 * ta, ta, R_R1});
+  EpiKktRow er{};
+  er.b = term_original ? B.b : B.b_s;
+  er.cy = cy;
+  er.m1 = (int)c->d.m1;
+  int ga = 0, gat = 0;
+  int rc = launch_sell(c, c->mat_a(!term_original), cx, er, P.krow, &ga);
+  if (rc) return rc;
+  EpiKktCol ec{};
+  ec.c = term_original ? B.c : B.c_s;
+  ec.lo = term_original ? B.lower : B.lower_s;
+  ec.up = term_original ? B.upper : B.upper_s;
+  ec.cx = cx;
+  ec.cz = cz;
+  rc = launch_sell(c, c->mat_at(!term_original), cy, ec, P.kcol, &gat);
+  if (rc) return rc;
+  segs.push_back({P.krow + 0 * ga, ga, R_PRIM2});
+  segs.push_back({P.krow + 1 * ga, ga, R_BY});
+  segs.push_back({P.krow + 2 * ga, ga, R_R1});
   const int outs[8] = {R_DUAL2, R_CX, R_LZ, R_UZ, R_NLO, R_NUP, R_CLAMP, R_R2};
-  for (int q = 0; q < 8; ++q) segs.push_back({P.kcol + q * tat, tat, outs[q]});
+  for (int q = 0; q < 8; ++q) segs.push_back({P.kcol + q * gat, gat, outs[q]});
   return HPR_OK;
 }
 
-int check_ctx(hpr_ctx *c, bool need_analyzed = true, bool need_scaled = false) {
+int check_ctx(hpr_ctx *c, bool need_layout = true, bool need_scaled = false) {
   if (!c) return fail(HPR_EINVAL, "null context");
   if (!c->bound) return fail(HPR_ESTATE, "hpr_bind has not been called");
-  if (need_analyzed && !c->analyzed) return fail(HPR_ESTATE, "hpr_analyze has not been called");
+  if (need_layout && !c->laid_out)
+    return fail(HPR_ESTATE, "hpr_analyze + hpr_bind_layout have not been called");
   if (need_scaled && !c->scaled) return fail(HPR_ESTATE, "hpr_scale has not been called");
+  return HPR_OK;
+}
+
+int kkt_common(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
+  const hpr_buffers &B = c->B;
+  std::vector<RedSeg> segs;
+  int rc = launch_kkt(c, term_original, B.cand_y[slot], B.cand_x[slot], B.cand_z[slot], segs);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, c->stream));
+  rc = reduce_final(c, segs);
+  if (rc) return rc;
+  rc = fetch_results(c);
+  if (rc) return rc;
+  fill_out(c, out);
   return HPR_OK;
 }
 
@@ -304,7 +389,7 @@ int hpr_workspace_bytes(const hpr_dims *dims, size_t *bytes) {
   if (!dims || !bytes) return fail(HPR_EINVAL, "null argument");
   if (dims->m < 1 || dims->n < 1 || dims->nnz < 0 || dims->m1 < 0 || dims->m1 > dims->m)
     return fail(HPR_EINVAL, "invalid dims");
-  if (dims->nnz >= INT_MAX || dims->m >= INT_MAX || dims->n >= INT_MAX)
+  if (dims->nnz >= INT_MAX || dims->m >= INT_MAX - kWindow || dims->n >= INT_MAX - kWindow)
     return fail(HPR_EINVAL, "dims exceed int32 indexing");
   size_t cb = 0;
   int rc = cub_temp_bytes(*dims, &cb);
@@ -328,14 +413,11 @@ int hpr_ctx_create(hpr_ctx **out, const hpr_dims *dims, int device, void *stream
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev2);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev3);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
     hpr_ctx_destroy(c);
     return fail(HPR_ECUDA, std::string("ctx_create: ") + cudaGetErrorString(e));
-  }
-  int rc = set_smem_attrs();
-  if (rc) {
-    hpr_ctx_destroy(c);
-    return rc;
   }
   *out = c;
   return HPR_OK;
@@ -371,12 +453,10 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
                        bufs->wtmp, bufs->cand_y[0], bufs->cand_y[1], bufs->cand_x[0],
                        bufs->cand_x[1], bufs->cand_z[0], bufs->cand_z[1]};
   for (const void *p : req)
-    if (!p && c->d.nnz > 0) return fail(HPR_EINVAL, "a required buffer pointer is null");
+    if (!p) return fail(HPR_EINVAL, "a required buffer pointer is null");
   c->B = *bufs;
   c->ws = (char *)workspace;
   c->L = L;
-  c->tiles_a = (int *)(c->ws + L.tiles_a);
-  c->tiles_at = (int *)(c->ws + L.tiles_at);
   c->part = (double *)(c->ws + L.part);
   c->results = (double *)(c->ws + L.results);
   c->fac = (double *)(c->ws + L.fac);
@@ -391,13 +471,14 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
     c->pow_graph = nullptr;
   }
   c->bound = true;
-  c->analyzed = c->scaled = false;
+  c->analyzed = c->laid_out = c->scaled = false;
   return HPR_OK;
 }
 
-int hpr_analyze(hpr_ctx *c) {
+int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   int rc = check_ctx(c, false);
   if (rc) return rc;
+  if (!layout_bytes) return fail(HPR_EINVAL, "null layout_bytes");
   CK(cudaSetDevice(c->device));
   const hpr_dims &d = c->d;
   const hpr_buffers &B = c->B;
@@ -428,13 +509,39 @@ int hpr_analyze(hpr_ctx *c) {
     CKL();
     c->launches += 1;
   }
-  rc = build_tiles(c, B.a_rp, m, c->tiles_a, &c->ntiles_a);
+  rc = plan_sell(c, c->L.pa, B.a_rp, m, c->sa);
   if (rc) return rc;
-  rc = build_tiles(c, B.at_rp, n, c->tiles_at, &c->ntiles_at);
+  rc = plan_sell(c, c->L.pat, B.at_rp, n, c->sat);
   if (rc) return rc;
-  if (c->ntiles_a > tile_bound(m, nnz) || c->ntiles_at > tile_bound(n, nnz))
-    return fail(HPR_ESTATE, "tile count exceeds its bound");
+  *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz);
   c->analyzed = true;
+  c->laid_out = false;
+  return HPR_OK;
+}
+
+int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
+  int rc = check_ctx(c, false);
+  if (rc) return rc;
+  if (!c->analyzed) return fail(HPR_ESTATE, "hpr_analyze has not been called");
+  if (!layout) return fail(HPR_EINVAL, "null layout");
+  if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz))
+    return fail(HPR_EINVAL, "layout buffer too small");
+  CK(cudaSetDevice(c->device));
+  const hpr_buffers &B = c->B;
+  char *p = (char *)layout;
+  rc = layout_sell(c, p, c->sa, B.a_rp, B.a_ci, B.a_val);
+  if (rc) return rc;
+  rc = layout_sell(c, p, c->sat, B.at_rp, B.at_ci, B.at_val);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
+  c->inner_graphs.clear();
+  if (c->pow_graph) {
+    cudaGraphExecDestroy(c->pow_graph);
+    c->pow_graph = nullptr;
+  }
+  c->laid_out = true;
+  c->scaled = false;
   return HPR_OK;
 }
 
@@ -482,34 +589,39 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
   if (bc_normalize) {  // sparse.py:245-250, scaling.py:98-101
     const int nb0 = sumsq_blocks(m), nb1 = sumsq_blocks(n);
     k_sumsq<<<nb0, kThreads, 0, s>>>(B.b_s, m, P.misc);
-    k_sumsq<<<nb1, kThreads, 0, s>>>(B.c_s, n, P.misc + 1024);
+    k_sumsq<<<nb1, kThreads, 0, s>>>(B.c_s, n, P.misc + kSumsqBlocks);
     CKL();
     c->launches += 2;
-    rc = reduce_final(c, {RedSeg{P.misc, nb0, R_SUMSQ0}, RedSeg{P.misc + 1024, nb1, R_SUMSQ1}});
+    rc = reduce_final(c, {RedSeg{P.misc, nb0, R_SUMSQ0},
+                          RedSeg{P.misc + kSumsqBlocks, nb1, R_SUMSQ1}});
     if (rc) return rc;
     k_factors<<<1, 32, 0, s>>>(c->results + R_SUMSQ0, c->fac);
     k_bc_normalize<<<g, 256, 0, s>>>(B.b_s, m, B.c_s, B.lower_s, B.upper_s, n, c->fac);
     CKL();
     c->launches += 2;
   } else {
-    const double ones[2] = {1.0, 1.0};
-    CK(cudaMemcpyAsync(c->fac, ones, sizeof(ones), cudaMemcpyHostToDevice, s));
+    k_fill<<<1, 32, 0, s>>>(c->fac, 1.0, 2);
+    CKL();
   }
   if (nnz > 0) {
     k_gather_vals<<<grid_for(nnz), 256, 0, s>>>(B.at_perm, B.a_val_s, B.at_val_s, nnz);
+    k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sa.pos, B.a_val_s, c->sa.val_s, nnz);
+    k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sat.pos, B.at_val_s, c->sat.val_s, nnz);
     CKL();
-    c->launches += 1;
+    c->launches += 3;
   }
   // ||b||, ||c|| of the original and the scaled problem (relative residual denominators)
   const int nbm = sumsq_blocks(m), nbn = sumsq_blocks(n);
   k_sumsq<<<nbm, kThreads, 0, s>>>(B.b, m, P.misc);
-  k_sumsq<<<nbn, kThreads, 0, s>>>(B.c, n, P.misc + 1024);
-  k_sumsq<<<nbm, kThreads, 0, s>>>(B.b_s, m, P.misc + 2048);
-  k_sumsq<<<nbn, kThreads, 0, s>>>(B.c_s, n, P.misc + 3072);
+  k_sumsq<<<nbn, kThreads, 0, s>>>(B.c, n, P.misc + kSumsqBlocks);
+  k_sumsq<<<nbm, kThreads, 0, s>>>(B.b_s, m, P.misc + 2 * kSumsqBlocks);
+  k_sumsq<<<nbn, kThreads, 0, s>>>(B.c_s, n, P.misc + 3 * kSumsqBlocks);
   CKL();
   c->launches += 4;
-  rc = reduce_final(c, {RedSeg{P.misc, nbm, R_SUMSQ0}, RedSeg{P.misc + 1024, nbn, R_SUMSQ1},
-                        RedSeg{P.misc + 2048, nbm, R_SUMSQ2}, RedSeg{P.misc + 3072, nbn, R_SUMSQ3}});
+  rc = reduce_final(c, {RedSeg{P.misc, nbm, R_SUMSQ0},
+                        RedSeg{P.misc + kSumsqBlocks, nbn, R_SUMSQ1},
+                        RedSeg{P.misc + 2 * kSumsqBlocks, nbm, R_SUMSQ2},
+                        RedSeg{P.misc + 3 * kSumsqBlocks, nbn, R_SUMSQ3}});
   if (rc) return rc;
   double fac[2];
   CK(cudaMemcpyAsync(fac, c->fac, sizeof(fac), cudaMemcpyDeviceToHost, s));
@@ -534,14 +646,20 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
   if (c->d.nnz == 0) return fail(HPR_EINVAL, "matrix must be non-zero");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
-  const int m = (int)c->d.m, n = (int)c->d.n;
+  const int m = (int)c->d.m;
   cudaStream_t s = c->stream;
   double *v = B.yb, *u = B.wtmp, *wv = B.dy;   // scratch reuse (before the iterations)
   Parts P = parts_of(c);
-  const size_t sm = hpr_ctx::smem();
   PowState st{};
   st.tol = tol;
   st.max_iters = max_iters;
+  EpiPowT et{};
+  et.u = u;
+  et.S = c->pow;
+  EpiPowA ea{};
+  ea.v = v;
+  ea.wv = wv;
+  ea.S = c->pow;
   // all-ones start; fall back to basis vectors while A^T v == 0 (sparse.py:176-182)
   int start = -2;
   for (int fb = -1; fb < m; ++fb) {
@@ -549,15 +667,13 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
       k_fill<<<grid_for(m), 256, 0, s>>>(v, 1.0, m);
     } else {
       k_fill<<<grid_for(m), 256, 0, s>>>(v, 0.0, m);
-      const double one = 1.0;
-      CK(cudaMemcpyAsync(v + fb, &one, sizeof(double), cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));   // `one` lives on this stack frame
+      k_fill<<<1, 32, 0, s>>>(v + fb, 1.0, 1);
     }
     CK(cudaMemcpyAsync(c->pow, &st, sizeof(st), cudaMemcpyHostToDevice, s));
-    k_pow_t<<<c->ntiles_at, kThreads, sm, s>>>(c->mat_at(B.at_val_s), v, u, c->pow, P.misc);
-    CKL();
-    c->launches += 2;
-    rc = reduce_final(c, {RedSeg{P.misc, c->ntiles_at, R_POW_U2}});
+    int gt = 0;
+    rc = launch_sell(c, c->mat_at(true), v, et, P.powt, &gt);
+    if (rc) return rc;
+    rc = reduce_final(c, {RedSeg{P.powt, gt, R_POW_U2}});
     if (rc) return rc;
     rc = fetch_results(c);
     if (rc) return rc;
@@ -584,12 +700,17 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
   }
   if (!c->pow_graph) {
     cudaGraph_t g;
+    const long long before = c->launches;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < kPowBatch; ++i) {
-      k_pow_t<<<c->ntiles_at, kThreads, sm, s>>>(c->mat_at(B.at_val_s), v, u, c->pow, P.misc);
-      k_pow_a<<<c->ntiles_a, kThreads, sm, s>>>(c->mat_a(B.a_val_s), u, v, wv, c->pow,
-                                                P.misc + c->ntiles_at);
-      k_pow_step<<<1, kThreads, 0, s>>>(P.misc + c->ntiles_at, c->ntiles_a, c->pow);
+      int ga = 0;
+      rc = launch_sell(c, c->mat_at(true), v, et, P.powt, nullptr);
+      if (!rc) rc = launch_sell(c, c->mat_a(true), u, ea, P.powa, &ga);
+      if (rc) {
+        cudaStreamEndCapture(s, &g);
+        return rc;
+      }
+      k_pow_step<<<1, kThreads, 0, s>>>(P.powa, ga, c->pow);
       k_pow_norm<<<grid_for(m), 256, 0, s>>>(wv, v, m, c->pow);
       k_pow_norm_done<<<1, 1, 0, s>>>(c->pow);
     }
@@ -597,7 +718,9 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
     if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("pow capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&c->pow_graph, g, 0);
     cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("pow instantiate: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess)
+      return fail(HPR_ECUDA, std::string("pow instantiate: ") + cudaGetErrorString(e));
+    c->launches = before;   // captured, not executed
   }
   for (;;) {
     CK(cudaGraphLaunch(c->pow_graph, s));
@@ -610,7 +733,6 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
   out->value = c->h_pow->lam * (1.0 + 1e-3);
   out->iterations = c->h_pow->iters;
   out->converged = c->h_pow->converged;
-  (void)n;
   return HPR_OK;
 }
 
@@ -626,9 +748,8 @@ int hpr_state_reset(hpr_ctx *c) {
   CK(cudaMemsetAsync(B.x, 0, nb, s));
   CK(cudaMemsetAsync(B.anc_x, 0, nb, s));
   CK(cudaMemsetAsync(B.w, 0, nb, s));
-  IterParams p{};
-  p.nonfinite_k = ULLONG_MAX;
-  CK(cudaMemcpyAsync(c->params, &p, sizeof(p), cudaMemcpyHostToDevice, s));
+  k_reset_params<<<1, 1, 0, s>>>(c->params);
+  CKL();
   CK(cudaStreamSynchronize(s));
   return HPR_OK;
 }
@@ -644,23 +765,42 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
   cudaStream_t s = c->stream;
   auto it = c->inner_graphs.find(steps);
   if (it == c->inner_graphs.end()) {
-    const size_t sm = hpr_ctx::smem();
-    const TileMat A = c->mat_a(B.a_val_s), AT = c->mat_at(B.at_val_s);
+    const SellMat A = c->mat_a(true), AT = c->mat_at(true);
+    EpiXIter ex{};
+    ex.c = B.c_s;
+    ex.lo = B.lower_s;
+    ex.up = B.upper_s;
+    ex.anc = B.anc_x;
+    ex.x = B.x;
+    ex.w = B.w;
+    ex.P = c->params;
+    EpiYIter ey{};
+    ey.b = B.b_s;
+    ey.anc = B.anc_y;
+    ey.y = B.y;
+    ey.P = c->params;
+    ey.m1 = (int)c->d.m1;
     cudaGraph_t g;
+    const long long before = c->launches;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < steps; ++i) {
-      k_x_iter<<<c->ntiles_at, kThreads, sm, s>>>(AT, B.y, B.x, B.w, B.c_s, B.lower_s,
-                                                  B.upper_s, B.anc_x, c->params, i);
-      k_y_iter<<<c->ntiles_a, kThreads, sm, s>>>(A, B.w, B.y, B.b_s, B.anc_y, (int)c->d.m1,
-                                                 c->params, i);
+      ex.step = i;
+      ey.step = i;
+      int rc2 = launch_sell(c, AT, B.y, ex, nullptr, nullptr);
+      if (!rc2) rc2 = launch_sell(c, A, B.w, ey, nullptr, nullptr);
+      if (rc2) {
+        cudaStreamEndCapture(s, &g);
+        return rc2;
+      }
     }
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
-    cudaGraphExec_t ex;
-    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphExec_t exe;
+    e = cudaGraphInstantiate(&exe, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
-    it = c->inner_graphs.emplace(steps, ex).first;
+    c->launches = before;   // captured, not executed
+    it = c->inner_graphs.emplace(steps, exe).first;
   }
   k_set_params<<<1, 1, 0, s>>>(c->params, sigma, lamsig, (long long)t, (long long)k, variant);
   CKL();
@@ -680,30 +820,50 @@ int hpr_checkpoint(hpr_ctx *c, double sigma, double lamsig, int term_original, i
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
   cudaStream_t s = c->stream;
-  const size_t sm = hpr_ctx::smem();
   Parts P = parts_of(c);
   CandCtx cc{term_original, c->fac, B.row_scale, B.col_scale, B.lower, B.upper};
   CK(cudaEventRecord(c->ev2, s));
-  k_x_half<<<c->ntiles_at, kThreads, sm, s>>>(c->mat_at(B.at_val_s), B.y, B.x, B.c_s, B.lower_s,
-                                              B.upper_s, B.anc_x, B.xb, B.zb, B.wtmp,
-                                              B.cand_x[slot], B.cand_z[slot], cc, sigma, P.xhalf);
-  CKL();
-  k_y_half<<<c->ntiles_a, kThreads, sm, s>>>(c->mat_a(B.a_val_s), B.wtmp, B.y, B.b_s, B.anc_y,
-                                             (int)c->d.m1, lamsig, B.yb, B.dy, B.cand_y[slot], cc,
-                                             P.yhalf);
-  CKL();
-  k_merit_col<<<c->ntiles_at, kThreads, sm, s>>>(c->mat_at(B.at_val_s), B.dy, B.x, B.xb, sigma,
-                                                 P.merit);
-  CKL();
-  c->launches += 3;
+  EpiXHalf ex{};
+  ex.x = B.x;
+  ex.c = B.c_s;
+  ex.lo = B.lower_s;
+  ex.up = B.upper_s;
+  ex.anc = B.anc_x;
+  ex.xb_out = B.xb;
+  ex.zb_out = B.zb;
+  ex.wtmp = B.wtmp;
+  ex.cx_out = B.cand_x[slot];
+  ex.cz_out = B.cand_z[slot];
+  ex.cc = cc;
+  ex.sigma = sigma;
+  int gx = 0, gy = 0, gm = 0;
+  rc = launch_sell(c, c->mat_at(true), B.y, ex, P.xhalf, &gx);
+  if (rc) return rc;
+  EpiYHalf ey{};
+  ey.y = B.y;
+  ey.b = B.b_s;
+  ey.anc = B.anc_y;
+  ey.yb_out = B.yb;
+  ey.dy_out = B.dy;
+  ey.cy_out = B.cand_y[slot];
+  ey.cc = cc;
+  ey.lamsig = lamsig;
+  ey.m1 = (int)c->d.m1;
+  rc = launch_sell(c, c->mat_a(true), B.wtmp, ey, P.yhalf, &gy);
+  if (rc) return rc;
+  EpiMeritCol em{};
+  em.x = B.x;
+  em.xb = B.xb;
+  em.sigma = sigma;
+  rc = launch_sell(c, c->mat_at(true), B.dy, em, P.merit, &gm);
+  if (rc) return rc;
   std::vector<RedSeg> segs;
-  const int ta = c->ntiles_a, tat = c->ntiles_at;
-  segs.push_back({P.xhalf, tat, R_BAR_DX2});
-  segs.push_back({P.xhalf + tat, tat, R_DX2});
-  segs.push_back({P.yhalf, ta, R_DY2});
-  segs.push_back({P.yhalf + ta, ta, R_BAR_DY2});
-  segs.push_back({P.merit, tat, R_SH2});
-  segs.push_back({P.merit + tat, tat, R_ATY2});
+  segs.push_back({P.xhalf, gx, R_BAR_DX2});
+  segs.push_back({P.xhalf + gx, gx, R_DX2});
+  segs.push_back({P.yhalf, gy, R_DY2});
+  segs.push_back({P.yhalf + gy, gy, R_BAR_DY2});
+  segs.push_back({P.merit, gm, R_SH2});
+  segs.push_back({P.merit + gm, gm, R_ATY2});
   rc = launch_kkt(c, term_original, B.cand_y[slot], B.cand_x[slot], B.cand_z[slot], segs);
   if (rc) return rc;
   rc = reduce_final(c, segs);
@@ -736,23 +896,13 @@ int hpr_kkt_origin(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
   if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
-  cudaStream_t s = c->stream;
   const int m = (int)c->d.m, n = (int)c->d.n;
-  k_origin_cand<<<grid_for(std::max(m, n)), 256, 0, s>>>(
+  k_origin_cand<<<grid_for(std::max(m, n)), 256, 0, c->stream>>>(
       B.cand_y[slot], m, B.cand_z[slot], B.cand_x[slot], term_original ? B.lower : B.lower_s,
       term_original ? B.upper : B.upper_s, n);
   CKL();
   c->launches += 1;
-  std::vector<RedSeg> segs;
-  rc = launch_kkt(c, term_original, B.cand_y[slot], B.cand_x[slot], B.cand_z[slot], segs);
-  if (rc) return rc;
-  CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, s));
-  rc = reduce_final(c, segs);
-  if (rc) return rc;
-  rc = fetch_results(c);
-  if (rc) return rc;
-  fill_out(c, out);
-  return HPR_OK;
+  return kkt_common(c, term_original, slot, out);
 }
 
 int hpr_kkt(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
@@ -760,17 +910,7 @@ int hpr_kkt(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
   if (rc) return rc;
   if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
   CK(cudaSetDevice(c->device));
-  const hpr_buffers &B = c->B;
-  std::vector<RedSeg> segs;
-  rc = launch_kkt(c, term_original, B.cand_y[slot], B.cand_x[slot], B.cand_z[slot], segs);
-  if (rc) return rc;
-  CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, c->stream));
-  rc = reduce_final(c, segs);
-  if (rc) return rc;
-  rc = fetch_results(c);
-  if (rc) return rc;
-  fill_out(c, out);
-  return HPR_OK;
+  return kkt_common(c, term_original, slot, out);
 }
 
 int hpr_finalize(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
@@ -779,27 +919,17 @@ int hpr_finalize(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
   if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
-  cudaStream_t s = c->stream;
   const int m = (int)c->d.m, n = (int)c->d.n;
   int fs = slot;
   if (!term_original) {
     fs = 1 - slot;
-    k_unscale<<<grid_for(std::max(m, n)), 256, 0, s>>>(
+    k_unscale<<<grid_for(std::max(m, n)), 256, 0, c->stream>>>(
         B.cand_y[slot], B.cand_z[slot], B.cand_x[slot], B.cand_y[fs], B.cand_z[fs],
         B.cand_x[fs], B.row_scale, B.col_scale, c->fac, B.lower, B.upper, m, n);
     CKL();
     c->launches += 1;
   }
-  std::vector<RedSeg> segs;
-  rc = launch_kkt(c, 1, B.cand_y[fs], B.cand_x[fs], B.cand_z[fs], segs);
-  if (rc) return rc;
-  CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, s));
-  rc = reduce_final(c, segs);
-  if (rc) return rc;
-  rc = fetch_results(c);
-  if (rc) return rc;
-  fill_out(c, out);
-  return HPR_OK;
+  return kkt_common(c, 1, fs, out);
 }
 
 int hpr_launch_count(hpr_ctx *c, int64_t *count) {
@@ -808,10 +938,14 @@ int hpr_launch_count(hpr_ctx *c, int64_t *count) {
   return HPR_OK;
 }
 
-int hpr_tile_info(hpr_ctx *c, int64_t *ntiles_a, int64_t *ntiles_at) {
-  if (!c || !ntiles_a || !ntiles_at) return fail(HPR_EINVAL, "null argument");
-  *ntiles_a = c->ntiles_a;
-  *ntiles_at = c->ntiles_at;
+int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
+  if (!c || !info) return fail(HPR_EINVAL, "null argument");
+  info->slices_a = c->sa.nslices;
+  info->slices_at = c->sat.nslices;
+  info->slots_a = c->sa.slots;
+  info->slots_at = c->sat.slots;
+  info->long_rows_a = c->sa.nlong;
+  info->long_rows_at = c->sat.nlong;
   return HPR_OK;
 }
 

@@ -54,14 +54,33 @@ __device__ __forceinline__ int ld_stream(const int *ptr, uint64_t pol) {
   return v;
 }
 
-struct TileMat {
-  const int *rp;        // nrows + 1
-  const int *ci;        // nnz
-  const double *val;    // nnz
-  const int *tile_row;  // ntiles + 1
-  int ntiles;
-  int cap;              // max nonzeros per (short-row) tile = smem products
+// Device layout of one matrix for the iteration kernels: SELL-32-sigma.
+// Rows are grouped in slices of 32 (lane i of a warp owns one row); inside a
+// window of kWindow rows they are ordered by decreasing length so a slice's
+// rows have similar lengths.  A slice stores its entries column-major
+// (entry k of all 32 rows is contiguous), so the warp's loads of values and
+// column indices are fully coalesced while each lane still adds its own row's
+// products in the CSR (ascending-column) order -- the reference's order.
+// Rows longer than kLongRow are kept out of the slices and summed by a whole
+// warp from the CSR arrays (same order).
+struct SellMat {
+  const int *slice_ptr;    // nslices + 1 (slot offsets)
+  const int *slice_row;    // nslices * 32: row of (slice, lane) or -1
+  const int *ci;           // slots
+  const double *val;       // slots
+  const int *rp;           // CSR row pointers
+  const int *csr_ci;       // CSR (for long rows)
+  const double *csr_val;
+  const int *long_rows;
+  int nslices;
+  int nlong;
 };
+
+constexpr int kSlice = 32;
+constexpr int kWindow = 256;            // sigma: sorting window (= one CTA's 8 slices)
+constexpr int kLongRow = 1024;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr int kUnroll = 4;
 
 // Parameters of the inner iterations, resident in device memory so a captured
 // graph replays with new sigma / counters without re-instantiation.
@@ -82,67 +101,102 @@ struct PowState {
 };
 
 // ---------------------------------------------------------------------------
-// products of one tile (or one chunk of a long row) into shared memory
+// TMA bulk copies + mbarrier (sm_90+ async proxy)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void tile_products(const TileMat &M, const double *__restrict__ xg,
-                                              int z0, int nz, double *sprod, uint64_t pol) {
-  int p = threadIdx.x;
-  // 4 independent gathers in flight per thread
-  for (; p + 3 * kThreads < nz; p += 4 * kThreads) {
-    int j0 = ld_stream(M.ci + z0 + p, pol);
-    int j1 = ld_stream(M.ci + z0 + p + kThreads, pol);
-    int j2 = ld_stream(M.ci + z0 + p + 2 * kThreads, pol);
-    int j3 = ld_stream(M.ci + z0 + p + 3 * kThreads, pol);
-    double a0 = ld_stream(M.val + z0 + p, pol);
-    double a1 = ld_stream(M.val + z0 + p + kThreads, pol);
-    double a2 = ld_stream(M.val + z0 + p + 2 * kThreads, pol);
-    double a3 = ld_stream(M.val + z0 + p + 3 * kThreads, pol);
-    double x0 = __ldg(xg + j0), x1 = __ldg(xg + j1), x2 = __ldg(xg + j2), x3 = __ldg(xg + j3);
-    sprod[pad_idx(p)] = __dmul_rn(a0, x0);
-    sprod[pad_idx(p + kThreads)] = __dmul_rn(a1, x1);
-    sprod[pad_idx(p + 2 * kThreads)] = __dmul_rn(a2, x2);
-    sprod[pad_idx(p + 3 * kThreads)] = __dmul_rn(a3, x3);
-  }
-  for (; p < nz; p += kThreads) {
-    int j = ld_stream(M.ci + z0 + p, pol);
-    double a = ld_stream(M.val + z0 + p, pol);
-    sprod[pad_idx(p)] = __dmul_rn(a, __ldg(xg + j));
-  }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
 }
 
-// Row sums of one tile.  Returns the sum for row `r` (owner thread) and whether
-// this thread owns a row.  Long single-row tiles are chunked; thread 0 keeps the
-// running left-to-right sum, so the order is still the sequential one.
-__device__ __forceinline__ double tile_row_sum(const TileMat &M, const double *__restrict__ xg,
-                                               double *sprod, int &r, bool &active) {
-  const uint64_t pol = policy_evict_first();
-  const int tile = blockIdx.x;
-  const int r0 = M.tile_row[tile], r1 = M.tile_row[tile + 1];
-  const int z0 = M.rp[r0];
-  const int nz = M.rp[r1] - z0;
-  double s = 0.0;
-  if (nz <= M.cap) {
-    tile_products(M, xg, z0, nz, sprod, pol);
-    __syncthreads();
-    r = r0 + threadIdx.x;
-    active = r < r1;
-    if (active) {
-      const int a = M.rp[r] - z0, e = M.rp[r + 1] - z0;
-      for (int k = a; k < e; ++k) s = __dadd_rn(s, sprod[pad_idx(k)]);
-    }
-  } else {
-    r = r0;
-    active = threadIdx.x == 0;
-    for (int c0 = 0; c0 < nz; c0 += M.cap) {
-      const int cn = min(M.cap, nz - c0);
-      tile_products(M, xg, z0 + c0, cn, sprod, pol);
-      __syncthreads();
-      if (threadIdx.x == 0)
-        for (int k = 0; k < cn; ++k) s = __dadd_rn(s, sprod[pad_idx(k)]);
-      __syncthreads();
+// ---------------------------------------------------------------------------
+// the SELL engine
+// ---------------------------------------------------------------------------
+// Epi (per-thread functor copy) provides
+//   static constexpr int NQ;                      reduction quantities (may be 0)
+//   bool enter();                                 uniform early-out (power method)
+//   void prefetch(int r);                         load the row's operand vectors
+//   void finish(int r, double s, double *acc);    fused elementwise + reduction terms
+template <class Epi>
+__device__ __forceinline__ void sell_slice(const SellMat &M, int s, int lane,
+                                           const double *__restrict__ xg, Epi &epi, double *acc,
+                                           uint64_t pol) {
+  const int row = M.slice_row[s * kSlice + lane];
+  const int base = M.slice_ptr[s];
+  const int slen = (M.slice_ptr[s + 1] - base) / kSlice;
+  int len = 0;
+  if (row >= 0) {
+    len = M.rp[row + 1] - M.rp[row];
+    epi.prefetch(row);
+  }
+  const int *cp = M.ci + base + lane;
+  const double *vp = M.val + base + lane;
+  double sum = 0.0;
+  for (int k = 0; k < slen; k += kUnroll) {
+    int c[kUnroll];
+    double v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < len) {
+        c[u] = ld_stream(cp + (k + u) * kSlice, pol);
+        v[u] = ld_stream(vp + (k + u) * kSlice, pol);
+      }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < len) xv[u] = __ldg(xg + c[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+  }
+  if (row >= 0) epi.finish(row, sum, acc);
+}
+
+// a long row: the warp forms 32 products at a time, lane 0 adds them in order
+template <class Epi>
+__device__ __forceinline__ void long_row(const SellMat &M, int row, int lane,
+                                         const double *__restrict__ xg, Epi &epi, double *acc,
+                                         uint64_t pol) {
+  if (lane == 0) epi.prefetch(row);
+  const int z0 = M.rp[row], z1 = M.rp[row + 1];
+  double sum = 0.0;
+  for (int c0 = z0; c0 < z1; c0 += 32) {
+    const int kk = c0 + lane;
+    double p = 0.0;
+    if (kk < z1) p = __dmul_rn(ld_stream(M.csr_val + kk, pol), __ldg(xg + ld_stream(M.csr_ci + kk, pol)));
+    const int cnt = min(32, z1 - c0);
+    for (int i = 0; i < cnt; ++i) {
+      const double q = __shfl_sync(0xffffffffu, p, i);
+      if (lane == 0) sum = __dadd_rn(sum, q);
     }
   }
-  return s;
+  if (lane == 0) epi.finish(row, sum, acc);
 }
 
 // Fixed-order block reduction of NQ values: the block totals end up in v[] of
@@ -190,208 +244,289 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
   wa = __ddiv_rn(1.0, t2);
 }
 
-__device__ __forceinline__ void mark_nonfinite(IterParams *P, long long k) {
-  atomicMin(&P->nonfinite_k, (unsigned long long)k);
-}
-
-// ---------------------------------------------------------------------------
-// inner iteration: x phase over A^T rows (core.py:168-169 + 149-153)
-// ---------------------------------------------------------------------------
+// One CTA = 8 warps; CTA c handles sorting windows c, c + G, ... (warp w takes
+// slice 8*window + w), then the long rows are strided over all warps.  Static
+// assignment keeps the per-CTA partial sums deterministic.
+template <class Epi>
 __global__ void __launch_bounds__(kThreads)
-k_x_iter(TileMat AT, const double *__restrict__ y, double *__restrict__ x, double *__restrict__ w,
-         const double *__restrict__ c, const double *__restrict__ lo, const double *__restrict__ up,
-         const double *__restrict__ anc_x, IterParams *P, int step) {
-  extern __shared__ double sprod[];
-  int j;
-  bool active;
-  const double aty = tile_row_sum(AT, y, sprod, j, active);
-  if (!active) return;
-  const double sigma = P->sigma;
-  const int variant = P->variant;
-  const long long t = P->t0 + step;
-  const double xj = x[j];
-  const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, c[j])));
-  const double xb = np_clip(v, lo[j], up[j]);
-  const double wj = __dsub_rn(__dmul_rn(2.0, xb), xj);
-  double xn;
-  if (variant == 0) {
-    xn = xb;
-  } else {
-    double wa, wn;
-    halpern_weights(t, wa, wn);
-    xn = __dadd_rn(__dmul_rn(wa, anc_x[j]), __dmul_rn(wn, variant == 2 ? wj : xb));
+k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
+  double acc[Epi::NQ > 0 ? Epi::NQ : 1];
+#pragma unroll
+  for (int q = 0; q < (Epi::NQ > 0 ? Epi::NQ : 1); ++q) acc[q] = 0.0;
+  if (!epi.enter()) return;
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  for (int win = blockIdx.x; win < nwin; win += gridDim.x) {
+    const int sl = win * kWarpsPerCta + wib;
+    if (sl < M.nslices) sell_slice(M, sl, lane, xg, epi, acc, pol);
   }
-  w[j] = wj;
-  x[j] = xn;
-  if (!isfinite(xn)) mark_nonfinite(P, P->k0 + step);
-}
-
-// y phase over A rows (core.py:170-172 + 149-153); y updated in place.
-__global__ void __launch_bounds__(kThreads)
-k_y_iter(TileMat A, const double *__restrict__ w, double *__restrict__ y,
-         const double *__restrict__ b, const double *__restrict__ anc_y, int m1, IterParams *P,
-         int step) {
-  extern __shared__ double sprod[];
-  int i;
-  bool active;
-  const double s = tile_row_sum(A, w, sprod, i, active);
-  if (!active) return;
-  const int variant = P->variant;
-  const long long t = P->t0 + step;
-  const double yi = y[i];
-  double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(b[i], s), P->lamsig));
-  if (i >= m1) yb = np_max(yb, 0.0);
-  double yn;
-  if (variant == 0) {
-    yn = yb;
-  } else {
-    double wa, wn;
-    halpern_weights(t, wa, wn);
-    const double tgt = variant == 2 ? __dsub_rn(__dmul_rn(2.0, yb), yi) : yb;
-    yn = __dadd_rn(__dmul_rn(wa, anc_y[i]), __dmul_rn(wn, tgt));
-  }
-  y[i] = yn;
-  if (!isfinite(yn)) mark_nonfinite(P, P->k0 + step);
+  for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += gridDim.x * kWarpsPerCta)
+    long_row(M, M.long_rows[li], lane, xg, epi, acc, pol);
+  if constexpr (Epi::NQ > 0) block_reduce_store<Epi::NQ>(acc, part, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
-// checkpoint kernels
+// inner iteration epilogues
+// ---------------------------------------------------------------------------
+// x phase over A^T rows (core.py:168-169 + 149-153): x updated in place,
+// w = 2 xb - x for the y phase.
+struct EpiXIter {
+  static constexpr int NQ = 0;
+  const double *c, *lo, *up, *anc;
+  double *x, *w;
+  IterParams *P;
+  int step;
+  double sigma, wa, wn, xj, cj, lj, uj, aj;
+  int variant;
+  __device__ bool enter() {
+    sigma = P->sigma;
+    variant = P->variant;
+    halpern_weights(P->t0 + step, wa, wn);
+    return true;
+  }
+  __device__ void prefetch(int j) {
+    xj = x[j];
+    cj = c[j];
+    lj = lo[j];
+    uj = up[j];
+    aj = variant ? anc[j] : 0.0;
+  }
+  __device__ void finish(int j, double aty, double *) {
+    const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cj)));
+    const double xb = np_clip(v, lj, uj);
+    const double wj = __dsub_rn(__dmul_rn(2.0, xb), xj);
+    const double xn =
+        variant == 0 ? xb : __dadd_rn(__dmul_rn(wa, aj), __dmul_rn(wn, variant == 2 ? wj : xb));
+    w[j] = wj;
+    x[j] = xn;
+    if (!isfinite(xn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
+  }
+};
+
+// y phase over A rows (core.py:170-172 + 149-153): y updated in place.
+struct EpiYIter {
+  static constexpr int NQ = 0;
+  const double *b, *anc;
+  double *y;
+  IterParams *P;
+  int step, m1;
+  double lamsig, wa, wn, yi, bi, ai;
+  int variant;
+  __device__ bool enter() {
+    lamsig = P->lamsig;
+    variant = P->variant;
+    halpern_weights(P->t0 + step, wa, wn);
+    return true;
+  }
+  __device__ void prefetch(int i) {
+    yi = y[i];
+    bi = b[i];
+    ai = variant ? anc[i] : 0.0;
+  }
+  __device__ void finish(int i, double s, double *) {
+    double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bi, s), lamsig));
+    if (i >= m1) yb = np_max(yb, 0.0);
+    double yn = yb;
+    if (variant != 0) {
+      const double tgt = variant == 2 ? __dsub_rn(__dmul_rn(2.0, yb), yi) : yb;
+      yn = __dadd_rn(__dmul_rn(wa, ai), __dmul_rn(wn, tgt));
+    }
+    y[i] = yn;
+    if (!isfinite(yn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// checkpoint epilogues
 // ---------------------------------------------------------------------------
 struct CandCtx {
   int term_original;
-  const double *b_factor_c_factor;   // device [bf, cf]
+  const double *fac;                 // device [b_factor, c_factor]
   const double *row_scale, *col_scale;
   const double *lo0, *up0;           // original bounds (clip target)
 };
 
 // half step x part (core.py:123-125) + candidate unscale/clip (scaling.py:46,48;
-// driver.py:334-336) + ||xb - anchor_x||^2 and ||x - xb||^2.
-__global__ void __launch_bounds__(kThreads)
-k_x_half(TileMat AT, const double *__restrict__ y, const double *__restrict__ x,
-         const double *__restrict__ c, const double *__restrict__ lo, const double *__restrict__ up,
-         const double *__restrict__ anc_x, double *__restrict__ xb_out, double *__restrict__ zb_out,
-         double *__restrict__ wtmp, double *__restrict__ cx_out, double *__restrict__ cz_out,
-         CandCtx cc, double sigma, double *part) {
-  extern __shared__ double sprod[];
-  int j;
-  bool active;
-  const double aty = tile_row_sum(AT, y, sprod, j, active);
-  double acc[2] = {0.0, 0.0};
-  if (active) {
-    const double xj = x[j];
-    const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, c[j])));
-    const double xb = np_clip(v, lo[j], up[j]);
+// driver.py:334-336); sums ||xb - anchor_x||^2, ||x - xb||^2.
+struct EpiXHalf {
+  static constexpr int NQ = 2;
+  const double *x, *c, *lo, *up, *anc;
+  double *xb_out, *zb_out, *wtmp, *cx_out, *cz_out;
+  CandCtx cc;
+  double sigma, bf, cf;
+  double xj, cj, lj, uj, aj, csj, l0, u0;
+  __device__ bool enter() {
+    bf = cc.fac[0];
+    cf = cc.fac[1];
+    return true;
+  }
+  __device__ void prefetch(int j) {
+    xj = x[j];
+    cj = c[j];
+    lj = lo[j];
+    uj = up[j];
+    aj = anc[j];
+    if (cc.term_original) {
+      csj = cc.col_scale[j];
+      l0 = cc.lo0[j];
+      u0 = cc.up0[j];
+    }
+  }
+  __device__ void finish(int j, double aty, double *acc) {
+    const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cj)));
+    const double xb = np_clip(v, lj, uj);
     const double zb = __ddiv_rn(__dsub_rn(xb, v), sigma);
     xb_out[j] = xb;
     zb_out[j] = zb;
     wtmp[j] = __dsub_rn(__dmul_rn(2.0, xb), xj);
-    acc[0] = sq(__dsub_rn(xb, anc_x[j]));
-    acc[1] = sq(__dsub_rn(xj, xb));
+    acc[0] = __dadd_rn(acc[0], sq(__dsub_rn(xb, aj)));
+    acc[1] = __dadd_rn(acc[1], sq(__dsub_rn(xj, xb)));
     if (cc.term_original) {
-      const double bf = cc.b_factor_c_factor[0], cf = cc.b_factor_c_factor[1];
-      const double cs = cc.col_scale[j];
-      cx_out[j] = np_clip(__dmul_rn(xb, __ddiv_rn(bf, cs)), cc.lo0[j], cc.up0[j]);
-      cz_out[j] = __dmul_rn(zb, __dmul_rn(cf, cs));
+      cx_out[j] = np_clip(__dmul_rn(xb, __ddiv_rn(bf, csj)), l0, u0);
+      cz_out[j] = __dmul_rn(zb, __dmul_rn(cf, csj));
     } else {
       cx_out[j] = xb;
       cz_out[j] = zb;
     }
   }
-  block_reduce_store<2>(acc, part, gridDim.x);
-}
+};
 
-// half step y part (core.py:126-128) + candidate y + ||y - yb||^2, ||yb - anchor_y||^2.
-__global__ void __launch_bounds__(kThreads)
-k_y_half(TileMat A, const double *__restrict__ wtmp, const double *__restrict__ y,
-         const double *__restrict__ b, const double *__restrict__ anc_y, int m1, double lamsig,
-         double *__restrict__ yb_out, double *__restrict__ dy_out, double *__restrict__ cy_out,
-         CandCtx cc, double *part) {
-  extern __shared__ double sprod[];
-  int i;
-  bool active;
-  const double s = tile_row_sum(A, wtmp, sprod, i, active);
-  double acc[2] = {0.0, 0.0};
-  if (active) {
-    const double yi = y[i];
-    double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(b[i], s), lamsig));
+// half step y part (core.py:126-128) + candidate y; sums ||y - yb||^2, ||yb - anchor_y||^2.
+struct EpiYHalf {
+  static constexpr int NQ = 2;
+  const double *y, *b, *anc;
+  double *yb_out, *dy_out, *cy_out;
+  CandCtx cc;
+  double lamsig, cf;
+  int m1;
+  double yi, bi, ai, rsi;
+  __device__ bool enter() {
+    cf = cc.fac[1];
+    return true;
+  }
+  __device__ void prefetch(int i) {
+    yi = y[i];
+    bi = b[i];
+    ai = anc[i];
+    if (cc.term_original) rsi = cc.row_scale[i];
+  }
+  __device__ void finish(int i, double s, double *acc) {
+    double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bi, s), lamsig));
     if (i >= m1) yb = np_max(yb, 0.0);
     const double dy = __dsub_rn(yi, yb);
     yb_out[i] = yb;
     dy_out[i] = dy;
-    acc[0] = sq(dy);
-    acc[1] = sq(__dsub_rn(yb, anc_y[i]));
-    cy_out[i] = cc.term_original
-                    ? __dmul_rn(yb, __ddiv_rn(cc.b_factor_c_factor[1], cc.row_scale[i]))
-                    : yb;
+    acc[0] = __dadd_rn(acc[0], sq(dy));
+    acc[1] = __dadd_rn(acc[1], sq(__dsub_rn(yb, ai)));
+    cy_out[i] = cc.term_original ? __dmul_rn(yb, __ddiv_rn(cf, rsi)) : yb;
   }
-  block_reduce_store<2>(acc, part, gridDim.x);
-}
+};
 
 // KKT row terms over the termination problem's A (driver.py:203-206, 211, 214).
-__global__ void __launch_bounds__(kThreads)
-k_kkt_row(TileMat A, const double *__restrict__ cx, const double *__restrict__ cy,
-          const double *__restrict__ b, int m1, double *part) {
-  extern __shared__ double sprod[];
-  int i;
-  bool active;
-  const double ax = tile_row_sum(A, cx, sprod, i, active);
-  double acc[3] = {0.0, 0.0, 0.0};
-  if (active) {
-    const double bi = b[i], yi = cy[i];
+struct EpiKktRow {
+  static constexpr int NQ = 3;
+  const double *b, *cy;
+  int m1;
+  double bi, yi;
+  __device__ bool enter() { return true; }
+  __device__ void prefetch(int i) {
+    bi = b[i];
+    yi = cy[i];
+  }
+  __device__ void finish(int i, double ax, double *acc) {
     double prim = __dsub_rn(bi, ax);
     double tproj = __dadd_rn(__dsub_rn(yi, ax), bi);
     if (i >= m1) {
       prim = np_max(prim, 0.0);
       tproj = np_max(tproj, 0.0);
     }
-    acc[0] = sq(prim);
-    acc[1] = __dmul_rn(bi, yi);
-    acc[2] = sq(__dsub_rn(yi, tproj));
+    acc[0] = __dadd_rn(acc[0], sq(prim));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(bi, yi));
+    acc[2] = __dadd_rn(acc[2], sq(__dsub_rn(yi, tproj)));
   }
-  block_reduce_store<3>(acc, part, gridDim.x);
-}
+};
 
 // KKT column terms over the termination problem's A^T (driver.py:207-215,
 // problem.py:146-176).
-__global__ void __launch_bounds__(kThreads)
-k_kkt_col(TileMat AT, const double *__restrict__ cy, const double *__restrict__ cx,
-          const double *__restrict__ cz, const double *__restrict__ c, const double *__restrict__ lo,
-          const double *__restrict__ up, double *part) {
-  extern __shared__ double sprod[];
-  int j;
-  bool active;
-  const double aty = tile_row_sum(AT, cy, sprod, j, active);
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (active) {
-    const double cj = c[j], zj = cz[j], xj = cx[j], l = lo[j], u = up[j];
-    acc[0] = sq(__dsub_rn(__dsub_rn(cj, aty), zj));
-    acc[1] = __dmul_rn(cj, xj);
-    if (zj > 0.0) {
-      if (isfinite(l)) { acc[2] = __dmul_rn(l, zj); acc[4] = 1.0; } else { acc[6] = 1.0; }
-    } else if (zj < 0.0) {
-      if (isfinite(u)) { acc[3] = __dmul_rn(u, zj); acc[5] = 1.0; } else { acc[6] = 1.0; }
-    }
-    acc[7] = sq(__dsub_rn(xj, np_clip(__dsub_rn(xj, zj), l, u)));
+struct EpiKktCol {
+  static constexpr int NQ = 8;
+  const double *c, *lo, *up, *cx, *cz;
+  double cj, zj, xj, l, u;
+  __device__ bool enter() { return true; }
+  __device__ void prefetch(int j) {
+    cj = c[j];
+    zj = cz[j];
+    xj = cx[j];
+    l = lo[j];
+    u = up[j];
   }
-  block_reduce_store<8>(acc, part, gridDim.x);
-}
+  __device__ void finish(int j, double aty, double *acc) {
+    acc[0] = __dadd_rn(acc[0], sq(__dsub_rn(__dsub_rn(cj, aty), zj)));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(cj, xj));
+    if (zj > 0.0) {
+      if (isfinite(l)) {
+        acc[2] = __dadd_rn(acc[2], __dmul_rn(l, zj));
+        acc[4] += 1.0;
+      } else {
+        acc[6] += 1.0;
+      }
+    } else if (zj < 0.0) {
+      if (isfinite(u)) {
+        acc[3] = __dadd_rn(acc[3], __dmul_rn(u, zj));
+        acc[5] += 1.0;
+      } else {
+        acc[6] += 1.0;
+      }
+    }
+    acc[7] = __dadd_rn(acc[7], sq(__dsub_rn(xj, np_clip(__dsub_rn(xj, zj), l, u))));
+  }
+};
 
 // merit terms over the scaled A^T (core.py:191-197): aty = A^T dy.
-__global__ void __launch_bounds__(kThreads)
-k_merit_col(TileMat AT, const double *__restrict__ dy, const double *__restrict__ x,
-            const double *__restrict__ xb, double sigma, double *part) {
-  extern __shared__ double sprod[];
-  int j;
-  bool active;
-  const double aty = tile_row_sum(AT, dy, sprod, j, active);
-  double acc[2] = {0.0, 0.0};
-  if (active) {
-    const double dx = __dsub_rn(x[j], xb[j]);
-    acc[0] = sq(__dadd_rn(dx, __dmul_rn(sigma, aty)));
-    acc[1] = sq(aty);
+struct EpiMeritCol {
+  static constexpr int NQ = 2;
+  const double *x, *xb;
+  double sigma, xj, xbj;
+  __device__ bool enter() { return true; }
+  __device__ void prefetch(int j) {
+    xj = x[j];
+    xbj = xb[j];
   }
-  block_reduce_store<2>(acc, part, gridDim.x);
-}
+  __device__ void finish(int j, double aty, double *acc) {
+    const double dx = __dsub_rn(xj, xbj);
+    acc[0] = __dadd_rn(acc[0], sq(__dadd_rn(dx, __dmul_rn(sigma, aty))));
+    acc[1] = __dadd_rn(acc[1], sq(aty));
+  }
+};
+
+// power method (sparse.py:189-191): u = A^T v (sum u^2 for the start check),
+// w = A u with v.w and w.w.
+struct EpiPowT {
+  static constexpr int NQ = 1;
+  double *u;
+  const PowState *S;
+  __device__ bool enter() { return !S->done; }
+  __device__ void prefetch(int) {}
+  __device__ void finish(int j, double s, double *acc) {
+    u[j] = s;
+    acc[0] = __dadd_rn(acc[0], sq(s));
+  }
+};
+struct EpiPowA {
+  static constexpr int NQ = 2;
+  const double *v;
+  double *wv;
+  const PowState *S;
+  double vi;
+  __device__ bool enter() { return !S->done; }
+  __device__ void prefetch(int i) { vi = v[i]; }
+  __device__ void finish(int i, double s, double *acc) {
+    wv[i] = s;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(vi, s));
+    acc[1] = __dadd_rn(acc[1], sq(s));
+  }
+};
 
 // ---------------------------------------------------------------------------
 // fixed-order final reduction: one CTA per segment
@@ -414,50 +549,14 @@ __global__ void __launch_bounds__(kThreads) k_reduce_final(RedList L, double *ou
   if (threadIdx.x == 0) out[sg.out] = a[0];
 }
 
-// ---------------------------------------------------------------------------
-// power method (sparse.py:176-198) -- all decisions on the device
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-k_pow_t(TileMat AT, const double *__restrict__ v, double *__restrict__ u, const PowState *S,
-        double *part) {
-  if (S->done) return;
-  extern __shared__ double sprod[];
-  int j;
-  bool active;
-  const double s = tile_row_sum(AT, v, sprod, j, active);
-  double acc[1] = {0.0};
-  if (active) {
-    u[j] = s;
-    acc[0] = sq(s);
-  }
-  block_reduce_store<1>(acc, part, gridDim.x);
-}
-
-__global__ void __launch_bounds__(kThreads)
-k_pow_a(TileMat A, const double *__restrict__ u, const double *__restrict__ v,
-        double *__restrict__ wv, const PowState *S, double *part) {
-  if (S->done) return;
-  extern __shared__ double sprod[];
-  int i;
-  bool active;
-  const double s = tile_row_sum(A, u, sprod, i, active);
-  double acc[2] = {0.0, 0.0};
-  if (active) {
-    wv[i] = s;
-    acc[0] = __dmul_rn(v[i], s);
-    acc[1] = sq(s);
-  }
-  block_reduce_store<2>(acc, part, gridDim.x);
-}
-
 // one CTA: reduce the v.w and w.w partials in fixed order, then the scalar
 // logic of one power step (sparse.py:188-198).
-__global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int ntiles, PowState *S) {
+__global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int nparts, PowState *S) {
   if (S->done) return;
   double a[2] = {0.0, 0.0};
-  for (int i = threadIdx.x; i < ntiles; i += kThreads) {
+  for (int i = threadIdx.x; i < nparts; i += kThreads) {
     a[0] = __dadd_rn(a[0], part[i]);
-    a[1] = __dadd_rn(a[1], part[ntiles + i]);
+    a[1] = __dadd_rn(a[1], part[nparts + i]);
   }
   block_reduce<2>(a);
   if (threadIdx.x == 0) {
@@ -535,29 +634,68 @@ __global__ void k_gather_t(const int *perm, const int *row_of, const double *val
   }
 }
 
-// tile boundaries: a new tile starts at row i if i is a multiple of kThreads
-// rows into ... (see analyze()): bucket change, row-group change, or a long row.
-__global__ void k_tile_flags(const int *rp, int nrows, int bucket, int long_len, int *flags) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
-    int f;
-    if (i == 0) {
-      f = 1;
-    } else {
-      const int len_i = rp[i + 1] - rp[i], len_p = rp[i] - rp[i - 1];
-      f = (i % kThreads == 0) || (rp[i] / bucket != rp[i - 1] / bucket) || (len_i > long_len) ||
-          (len_p > long_len);
+
+
+
+// SELL plan: CTA per window of kWindow rows.  Rows are ranked by (length desc,
+// index asc); long rows and padding go last with row = -1.  Writes slice_row
+// and the slot count of each slice (32 * longest row in it).
+__global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows, int sort_rows,
+                                                       int *slice_row, int *slice_slots,
+                                                       int *long_flag) {
+  __shared__ int key[kWindow];
+  __shared__ int skey[kWindow];
+  const int t = threadIdx.x;
+  const int r = blockIdx.x * kWindow + t;
+  int k = -2;
+  if (r < nrows) {
+    const int len = rp[r + 1] - rp[r];
+    k = len > kLongRow ? -1 : len;
+    long_flag[r] = len > kLongRow;
+  }
+  key[t] = k;
+  __syncthreads();
+  int rank = t;
+  if (sort_rows) {
+    rank = 0;
+    for (int j = 0; j < kWindow; ++j) {
+      const int kj = key[j];
+      rank += (kj > k) || (kj == k && j < t);
     }
-    flags[i] = f;
+  }
+  skey[rank] = k;
+  slice_row[blockIdx.x * kWindow + rank] = k >= 0 ? r : -1;
+  __syncthreads();
+  if (t < kWindow / kSlice) {
+    int mx = 0;
+    for (int i = 0; i < kSlice; ++i) mx = max(mx, skey[t * kSlice + i]);
+    slice_slots[blockIdx.x * (kWindow / kSlice) + t] = mx * kSlice;
   }
 }
 
-__global__ void k_tile_scatter(const int *flags, const int *pos, int nrows, int *tile_row) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
-    if (flags[i]) tile_row[pos[i]] = i;
-    if (i == nrows - 1) {
-      const int nt = pos[i] + flags[i];
-      tile_row[nt] = nrows;
+// fill slot column indices and the CSR -> slot map (warp per slice)
+__global__ void k_sell_fill(const int *rp, const int *ci, const int *slice_ptr,
+                            const int *slice_row, int nslices, int *sell_ci, int *sell_pos) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += nw) {
+    const int row = slice_row[s * kSlice + lane];
+    if (row < 0) continue;
+    const int z0 = rp[row], len = rp[row + 1] - z0, base = slice_ptr[s];
+    for (int k = 0; k < len; ++k) {
+      const int pos = base + k * kSlice + lane;
+      sell_ci[pos] = ci[z0 + k];
+      sell_pos[z0 + k] = pos;
     }
+  }
+}
+
+// CSR values -> slots (entries of long rows have sell_pos = -1)
+__global__ void k_sell_scatter(const int *sell_pos, const double *src, double *dst, long long nnz) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int p = sell_pos[k];
+    if (p >= 0) dst[p] = src[k];
   }
 }
 
@@ -685,6 +823,15 @@ __global__ void k_unscale(const double *sy, const double *sz, const double *sx, 
     ox[j] = np_clip(__dmul_rn(sx[j], __ddiv_rn(bf, c)), lo0[j], up0[j]);
     oz[j] = __dmul_rn(sz[j], __dmul_rn(cf, c));
   }
+}
+
+__global__ void k_reset_params(IterParams *P) {
+  P->sigma = 0.0;
+  P->lamsig = 0.0;
+  P->t0 = 0;
+  P->k0 = 0;
+  P->variant = 0;
+  P->nonfinite_k = ~0ULL;
 }
 
 __global__ void k_set_params(IterParams *P, double sigma, double lamsig, long long t0,

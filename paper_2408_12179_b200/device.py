@@ -25,6 +25,8 @@ import numpy as np
 from . import _native as N
 from .problem import stacked_arrays
 
+PAD = 8   # trailing slots on every nonzero array (16-byte bulk-copy rounding)
+
 
 def _torch():
     import torch
@@ -61,14 +63,16 @@ class DeviceLP:
             rhs = np.concatenate([np.asarray(problem.b_eq, np.float64),
                                   np.asarray(problem.b_ineq, np.float64)])
             T = {}
+            # nonzero arrays carry PAD trailing slots: the tile engine's bulk copies
+            # round every tile up to 16-byte boundaries
             T["a_rp"] = up(ro, np.int32)
-            T["a_ci"] = up(ci if nnz else np.zeros(1), np.int32)
-            T["a_val"] = up(v if nnz else np.zeros(1), np.float64)
+            T["a_ci"] = up(np.concatenate([ci, np.zeros(PAD)]), np.int32)
+            T["a_val"] = up(np.concatenate([v, np.zeros(PAD)]), np.float64)
             T["b"] = up(rhs, np.float64)
             T["c"] = up(problem.c, np.float64)
             T["lower"] = up(problem.lower, np.float64)
             T["upper"] = up(problem.upper, np.float64)
-            nz1 = max(nnz, 1)
+            nz1 = nnz + PAD
             T["a_val_s"] = torch.empty(nz1, **f64)
             T["at_rp"] = torch.empty(n + 1, **i32)
             T["at_ci"] = torch.empty(nz1, **i32)
@@ -107,7 +111,15 @@ class DeviceLP:
 
     # ------------------------------------------------------------------
     def analyze(self):
-        N.call("hpr_analyze", self.ctx)
+        """Transpose + SELL-32-sigma layout (hpr_analyze / hpr_bind_layout)."""
+        torch = _torch()
+        nbytes = ctypes.c_size_t(0)
+        N.call("hpr_analyze", self.ctx, ctypes.byref(nbytes))
+        with torch.cuda.stream(self.stream):
+            self.layout = torch.empty(max(int(nbytes.value), 16), dtype=torch.uint8,
+                                      device=self.device)
+        N.call("hpr_bind_layout", self.ctx, ctypes.c_void_p(self.layout.data_ptr()),
+               ctypes.c_size_t(self.layout.numel()))
         self.analyzed = True
 
     def scale(self, ruiz_iters: int, pock_chambolle: bool, bc_normalize: bool):
@@ -157,10 +169,10 @@ class DeviceLP:
         N.call("hpr_launch_count", self.ctx, ctypes.byref(v))
         return int(v.value)
 
-    def tile_info(self):
-        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
-        N.call("hpr_tile_info", self.ctx, ctypes.byref(a), ctypes.byref(b))
-        return int(a.value), int(b.value)
+    def layout_info(self) -> dict:
+        info = N.HprLayoutInfo()
+        N.call("hpr_layout_info", self.ctx, ctypes.byref(info))
+        return {f: int(getattr(info, f)) for f, _ in N.HprLayoutInfo._fields_}
 
     def last_times(self):
         a, b = ctypes.c_double(0), ctypes.c_double(0)
@@ -172,6 +184,8 @@ class DeviceLP:
 
     def to_host(self, name, slot=None):
         t = self.t[name] if slot is None else self.t[name][slot]
+        if name in ("a_ci", "a_val", "a_val_s", "at_ci", "at_perm", "at_val", "at_val_s"):
+            t = t[:self.nnz]
         self.stream.synchronize()
         return t.cpu().numpy()
 

@@ -410,14 +410,14 @@ def solve(problem, cfg=None, *, device: int = 0, dev: DeviceLP | None = None) ->
     solution = PrimalDualPoint(y=dev.to_host("cand_y", final_slot),
                                z=dev.to_host("cand_z", final_slot),
                                x=dev.to_host("cand_x", final_slot))
-    n_a, n_at = dev.tile_info()
+    layout = dev.layout_info()
     return SolveReport(
         status=status, primal_objective=pobj, dual_objective=dobj, kkt=res, iterations=k,
         restarts=r, restart_log=restart_log, timings=timings, solution=solution,
         sigma_final=sigma, lambda_estimate=lam,
         device_stats={"lambda_raw": est.raw, "power_iterations": est.iterations,
                       "b_factor": sc.b_factor, "c_factor": sc.c_factor,
-                      "launches": dev.launch_count(), "tiles_a": n_a, "tiles_at": n_at,
+                      "launches": dev.launch_count(), "layout": layout,
                       "h2d_bytes": dev.h2d_bytes})
 
 

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden reports.
+
+Bars (BASELINE.json north_star):
+* sparse products and the fused iteration: BIT-EXACT against the oracle on
+  the same scaled problem and lambda (the kernels sum each row left to right
+  with separately rounded products, like scipy's csr_matvec);
+* Ruiz / Pock-Chambolle values and scale vectors: bit-exact;
+* solves vs the reference's golden reports: identical status and iteration
+  count, identical restart triggers, objectives and the relative residual
+  fields within 1e-8 * max(1, |ref|);
+* first 100 iterates normwise within 1e-10 of the reference trajectory.
+"""
+
+import json
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2408_12179_b200 as P
+from conftest import GOLDEN, acceptance_suite, bounded_tiny_lp, one_d_problem, problem_from_dict
+from oracle import hprlp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8
+
+
+def _dev(prob, ruiz=10, pc=True, bc=True):
+    from paper_2408_12179_b200.device import DeviceLP
+    dev = DeviceLP(prob)
+    dev.analyze()
+    dev.scale(ruiz, pc, bc)
+    return dev
+
+
+def _oracle_on_device_scaling(dev, prob):
+    olp = O.OracleLP.from_problem(prob)
+    a = O.Csr(olp.a.rp, olp.a.ci, dev.to_host("a_val_s"), olp.n)
+    return O.OracleLP(a=a, b=dev.to_host("b_s"), c=dev.to_host("c_s"),
+                      lower=dev.to_host("lower_s"), upper=dev.to_host("upper_s"), m1=olp.m1)
+
+
+def _close(a, b, rel=TOL):
+    if not (np.isfinite(a) and np.isfinite(b)):
+        return (np.isnan(a) and np.isnan(b)) or a == b
+    return abs(a - b) <= rel * max(1.0, abs(b))
+
+
+def assert_report_parity(rep, g, name=""):
+    d = rep.to_json_dict(include_solution=False)
+    assert d["status"] == g["status"], name
+    assert d["iterations"] == g["iterations"], name
+    assert d["restarts"] == g["restarts"], name
+    assert [e["trigger"] for e in d["restart_log"]] == [e["trigger"] for e in g["restart_log"]], name
+    assert [e["tau"] for e in d["restart_log"]] == [e["tau"] for e in g["restart_log"]], name
+    assert _close(d["primal_objective"], g["primal_objective"]), (name, d["primal_objective"])
+    assert _close(d["dual_objective"], g["dual_objective"]), (name, d["dual_objective"])
+    for k in ("primal_infeas_rel", "dual_infeas_rel", "gap_rel"):
+        assert _close(d["kkt"][k], g["kkt"][k]), (name, k, d["kkt"][k], g["kkt"][k])
+    assert d["kkt"]["dual_clamped"] == g["kkt"]["dual_clamped"], name
+    assert _close(d["lambda_estimate"], g["lambda_estimate"], 1e-12), name
+
+
+# ---------------------------------------------------------------------------
+# kernels: bit-exact against the oracle
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("variant,code", [("hpr", 2), ("hdr", 1), ("dr", 0)])
+def test_iteration_bit_exact_c1(variant, code):
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    dev = _dev(prob)
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.83, lam,
+                 variant=variant)
+    dev.state_reset()
+    for k in range(100):
+        dev.run_inner(1, k, k, 0.83, lam * 0.83, code)
+        O.iterate_once(st, slp)
+        if k % 9 == 0 or k == 99:
+            assert np.array_equal(dev.to_host("y"), st.y), k
+            assert np.array_equal(dev.to_host("x"), st.x), k
+    # one graph replay of 100 iterations lands on the same bits
+    dev.state_reset()
+    dev.run_inner(100, 0, 0, 0.83, lam * 0.83, code)
+    assert np.array_equal(dev.to_host("y"), st.y)
+    assert np.array_equal(dev.to_host("x"), st.x)
+
+
+def test_scaling_and_power_vs_oracle():
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    dev = _dev(prob)
+    sc_scaled, info = O.scale_lp(O.OracleLP.from_problem(prob))
+    assert np.array_equal(dev.to_host("a_val_s"), sc_scaled.a.vals)
+    assert np.array_equal(dev.to_host("row_scale"), info.row_scale)
+    assert np.array_equal(dev.to_host("col_scale"), info.col_scale)
+    for name, ref in (("b_s", sc_scaled.b), ("c_s", sc_scaled.c)):
+        got = dev.to_host(name)
+        assert np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref))) <= 1e-15
+    est = dev.power(1e-4, 5000)
+    oest = O.power_lambda(sc_scaled)
+    assert est.iterations == oest.iterations and bool(est.converged) == oest.converged
+    assert abs(est.raw - oest.raw) <= 1e-13 * oest.raw
+    # the transpose matches csr_matrix(A.T) ordering
+    at = O.OracleLP.from_problem(prob).transpose()
+    assert np.array_equal(dev.to_host("at_rp"), at.rp)
+    assert np.array_equal(dev.to_host("at_ci"), at.ci)
+    assert np.array_equal(dev.to_host("at_perm"), at.perm)
+
+
+def test_c1_trajectory_vs_reference_golden():
+    """Normwise 1e-10 against the reference's own first 100 iterates (its
+    scaling/lambda differ from ours only through BLAS dot rounding)."""
+    d = np.load(f"{GOLDEN}/c1_golden.npz")
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    dev = _dev(prob)
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    dev.state_reset()
+    done = 0
+    for i, k in enumerate(d["snap_k"]):
+        dev.run_inner(int(k) - done, done, done, 1.0, lam, 2)
+        done = int(k)
+        y, x = dev.to_host("y"), dev.to_host("x")
+        ry, rx = d["snap_y"][i], d["snap_x"][i]
+        rel = np.sqrt(np.sum((y - ry) ** 2) + np.sum((x - rx) ** 2)) / np.sqrt(
+            np.sum(ry ** 2) + np.sum(rx ** 2))
+        assert rel <= 1e-10, (k, rel)
+
+
+@pytest.mark.parametrize("shape", ["ineq_only", "eq_only", "empty_rows_cols", "long_rows",
+                                   "one_by_one"])
+def test_edge_shapes_bit_exact(shape):
+    rng = np.random.default_rng(7)
+    if shape == "ineq_only":
+        prob = P.LpProblem.from_dense(None, None, rng.uniform(-1, 1, (7, 5)), rng.uniform(-1, 0, 7),
+                                      rng.uniform(0, 1, 5))
+    elif shape == "eq_only":
+        prob, _ = P.generate_known_solution_lp(11, 6, 0, 12, 0.5)
+    elif shape == "empty_rows_cols":
+        a = rng.uniform(-1, 1, (40, 70))
+        a[rng.uniform(size=a.shape) < 0.7] = 0.0
+        a[5] = 0.0
+        a[:, 9] = 0.0
+        a[:, 33] = 0.0
+        prob = P.LpProblem.from_dense(a[:20], rng.uniform(-1, 1, 20), a[20:], rng.uniform(-1, 0, 20),
+                                      rng.uniform(-1, 1, 70), lower=-np.ones(70), upper=np.ones(70))
+    elif shape == "long_rows":
+        # rows of 300 / 1100 / 2600 nonzeros span 2..11 chunks; one dense column
+        n = 3000
+        rows, cols, vals = [], [], []
+        for i, ln in enumerate([300, 1100, 2600, 5, 7, 1]):
+            cc = np.sort(rng.choice(n, size=ln, replace=False))
+            rows += [i] * ln
+            cols += cc.tolist()
+            vals += rng.uniform(0.5, 2.0, ln).tolist()
+        for i in range(6, 60):
+            rows += [i, i]
+            cols += [17, (i * 37) % n]
+            vals += [1.0, -1.0]
+        a = P.SparseMatrix.from_coo(rows, cols, vals, (60, n))
+        dense = a.to_dense()
+        prob = P.LpProblem.from_dense(dense[:30], rng.uniform(-1, 1, 30), dense[30:],
+                                      rng.uniform(-1, 0, 30), rng.uniform(0, 1, n),
+                                      lower=np.zeros(n), upper=np.full(n, 3.0))
+    else:
+        prob = one_d_problem()
+    dev = _dev(prob)
+    est = dev.power(1e-4, 5000)
+    lam = est.raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    sc, _ = O.scale_lp(O.OracleLP.from_problem(prob))
+    assert np.array_equal(slp.a.vals, sc.a.vals)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 1.3, lam)
+    dev.state_reset()
+    dev.run_inner(60, 0, 0, 1.3, lam * 1.3, 2)
+    for _ in range(60):
+        O.iterate_once(st, slp)
+    assert np.array_equal(dev.to_host("y"), st.y)
+    assert np.array_equal(dev.to_host("x"), st.x)
+    rep = P.solve(prob, P.SolverConfig(tolerance=1e-6, max_iterations=3000))
+    ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(tolerance=1e-6, max_iterations=3000))
+    assert rep.status.value == ref["status"] and rep.iterations == ref["iterations"]
+    assert _close(rep.primal_objective, ref["primal_objective"])
+
+
+# ---------------------------------------------------------------------------
+# solves against the reference's golden reports
+# ---------------------------------------------------------------------------
+
+def test_acceptance_suite_vs_reference(golden_reports):
+    """SPEC acceptance criterion 2 instances at 1e-4 / 1e-6 / 1e-8 (60 solves)."""
+    for entry in golden_reports["acceptance_suite"]:
+        prob, _ = P.generate_known_solution_lp(*entry["args"])
+        rep = P.solve(prob, P.SolverConfig(**entry["cfg"]))
+        assert_report_parity(rep, entry["report"], str(entry["args"]) + str(entry["cfg"]["tolerance"]))
+        tol = entry["cfg"]["tolerance"]
+        assert max(rep.kkt.primal_infeas_rel, rep.kkt.dual_infeas_rel, rep.kkt.gap_rel) <= tol
+
+
+def test_small_cases_vs_reference(golden_reports):
+    """1-D, inequality-only, fixed / free variables, infeasible (iteration
+    limit), MAX flip, numerical breakdown, bounded tiny LPs, degenerate LPs
+    under all four variants, scaled termination space, no scaling,
+    check_interval 70 with an iteration limit."""
+    for case in golden_reports["small"]:
+        prob = problem_from_dict(case["problem"])
+        with warnings.catch_warnings(), np.errstate(all="ignore"):
+            warnings.simplefilter("ignore")
+            rep = P.solve(prob, P.SolverConfig(**case["cfg"]))
+        assert_report_parity(rep, case["report"], case["name"])
+
+
+def test_c1_vs_reference(golden_reports):
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    for key in ("c1", "c1_1e-8"):
+        g = golden_reports[key]
+        rep = P.solve(prob, P.SolverConfig(**g["cfg"]))
+        assert_report_parity(rep, g["report"], key)
+    d = np.load(f"{GOLDEN}/c1_golden.npz")
+    rep = P.solve(prob, P.SolverConfig(tolerance=1e-4))
+    assert np.allclose(rep.solution.x, d["sol_x"], rtol=1e-8, atol=1e-10)
+    assert np.allclose(rep.solution.y, d["sol_y"], rtol=1e-8, atol=1e-10)
+    assert np.allclose(rep.solution.z, d["sol_z"], rtol=1e-8, atol=1e-10)
+
+
+def test_c2_vs_reference(golden_reports):
+    """C2 (m=1e5, n=2e5, nnz=5e6) at 1e-8 against the reference's report."""
+    g = golden_reports["c2"]
+    prob, _ = P.generate_known_solution_lp(2, 50_000, 50_000, 200_000, 2.5e-4)
+    rep = P.solve(prob, P.SolverConfig(**g["cfg"]))
+    assert_report_parity(rep, g["report"], "c2")
+    for f in ("x", "y", "z"):
+        ref = g["report"]["solution_norm"][f]
+        assert abs(np.linalg.norm(getattr(rep.solution, f)) - ref) <= 1e-8 * max(1.0, ref)
+
+
+def test_determinism_bit_identical():
+    """SPEC acceptance criterion 10: repeated solves give identical reports."""
+    for spec in acceptance_suite()[:8]:
+        prob, _ = P.generate_known_solution_lp(*spec)
+        a = P.solve(prob, P.SolverConfig(tolerance=1e-6))
+        b = P.solve(prob, P.SolverConfig(tolerance=1e-6))
+        da, db = a.to_json_dict(), b.to_json_dict()
+        da.pop("timings")
+        db.pop("timings")
+        assert json.dumps(da, sort_keys=True) == json.dumps(db, sort_keys=True)
+
+
+def test_status_paths():
+    prob, _ = P.generate_known_solution_lp(12, 3, 3, 12, 0.4)
+    rep = P.solve(prob, P.SolverConfig(tolerance=1e-14, time_limit_seconds=0.0,
+                                       max_iterations=10**9))
+    assert rep.status is P.SolveStatus.TIME_LIMIT
+    rep = P.solve(one_d_problem(), P.SolverConfig(tolerance=1e-12, max_iterations=10))
+    assert rep.iterations <= 10
+    assert rep.status in (P.SolveStatus.ITERATION_LIMIT, P.SolveStatus.OPTIMAL)
+
+
+def test_reported_point_in_box_and_cone():
+    prob, pt = P.generate_known_solution_lp(2, 3, 2, 8, 0.5)
+    rep = P.solve(prob, P.SolverConfig(tolerance=1e-8))
+    assert rep.status is P.SolveStatus.OPTIMAL
+    assert np.all(rep.solution.x >= prob.lower) and np.all(rep.solution.x <= prob.upper)
+    assert np.all(rep.solution.y[prob.m1:] >= 0.0)
+    assert abs(rep.primal_objective - float(prob.c @ pt.x)) <= 1e-6 * max(1.0, abs(prob.c @ pt.x))
+
+
+def test_kkt_residual_vs_oracle():
+    prob = bounded_tiny_lp(21, n=5, m1=2, m2=2)
+    rng = np.random.default_rng(2)
+    pt = P.PrimalDualPoint(y=rng.normal(size=4), z=rng.normal(size=5), x=rng.normal(size=5))
+    got = P.kkt_residual(prob, pt).to_dict()
+    ref = O.kkt(O.OracleLP.from_problem(prob), pt.y, pt.z, pt.x)
+    for k, v in ref.items():
+        assert _close(got[k], v, 1e-12), k
