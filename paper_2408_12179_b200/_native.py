@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhprlp_b200.so")
+LIB_PATH = os.environ.get("HPR_LIB_PATH") or os.path.join(_HERE, "libhprlp_b200.so")
 
 HPR_OK = 0
 _ERRNAMES = {-1: "HPR_EINVAL", -2: "HPR_ECUDA", -3: "HPR_ENCCL", -4: "HPR_ENOMEM",

@@ -23,7 +23,7 @@
 
 namespace hpr {
 
-constexpr int kThreads = 256;           // CTA size of all tile kernels
+constexpr int kThreads = 128;           // CTA size of the SELL / reduction kernels
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ int pad_idx(int p) { return p + (p >> 4); }  // smem bank spread
@@ -77,10 +77,13 @@ struct SellMat {
 };
 
 constexpr int kSlice = 32;
-constexpr int kWindow = 256;            // sigma: sorting window (= one CTA's 8 slices)
+constexpr int kWindow = kThreads;       // sigma: sorting window (= one CTA's 4 slices)
 constexpr int kLongRow = 1024;
 constexpr int kWarpsPerCta = kThreads / 32;
-constexpr int kUnroll = 4;
+#ifndef HPR_UNROLL
+#define HPR_UNROLL 4
+#endif
+constexpr int kUnroll = HPR_UNROLL;     // entries per lane in flight (x2: software pipelined)
 
 // Parameters of the inner iterations, resident in device memory so a captured
 // graph replays with new sigma / counters without re-instantiation.
@@ -159,14 +162,24 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, int s, int lane,
   const int *cp = M.ci + base + lane;
   const double *vp = M.val + base + lane;
   double sum = 0.0;
+  // software pipeline: the streaming loads of batch i+1 are in flight while
+  // batch i's operand gathers complete and its products are added in order
+  int c[kUnroll];
+  double v[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (u < len) {
+      c[u] = ld_stream(cp + u * kSlice, pol);
+      v[u] = ld_stream(vp + u * kSlice, pol);
+    }
   for (int k = 0; k < slen; k += kUnroll) {
-    int c[kUnroll];
-    double v[kUnroll], xv[kUnroll];
+    int cn[kUnroll];
+    double vn[kUnroll], xv[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      if (k + u < len) {
-        c[u] = ld_stream(cp + (k + u) * kSlice, pol);
-        v[u] = ld_stream(vp + (k + u) * kSlice, pol);
+      if (k + kUnroll + u < len) {
+        cn[u] = ld_stream(cp + (k + kUnroll + u) * kSlice, pol);
+        vn[u] = ld_stream(vp + (k + kUnroll + u) * kSlice, pol);
       }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
@@ -174,6 +187,11 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, int s, int lane,
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
       if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      c[u] = cn[u];
+      v[u] = vn[u];
+    }
   }
   if (row >= 0) epi.finish(row, sum, acc);
 }

@@ -135,7 +135,7 @@ def test_edge_shapes_bit_exact(shape):
     rng = np.random.default_rng(7)
     if shape == "ineq_only":
         prob = P.LpProblem.from_dense(None, None, rng.uniform(-1, 1, (7, 5)), rng.uniform(-1, 0, 7),
-                                      rng.uniform(0, 1, 5))
+                                      rng.uniform(0, 1, 5), upper=np.full(5, 4.0))
     elif shape == "eq_only":
         prob, _ = P.generate_known_solution_lp(11, 6, 0, 12, 0.5)
     elif shape == "empty_rows_cols":
@@ -144,7 +144,8 @@ def test_edge_shapes_bit_exact(shape):
         a[5] = 0.0
         a[:, 9] = 0.0
         a[:, 33] = 0.0
-        prob = P.LpProblem.from_dense(a[:20], rng.uniform(-1, 1, 20), a[20:], rng.uniform(-1, 0, 20),
+        x0 = rng.uniform(-0.5, 0.5, 70)          # feasible by construction
+        prob = P.LpProblem.from_dense(a[:20], a[:20] @ x0, a[20:], a[20:] @ x0 - 0.1,
                                       rng.uniform(-1, 1, 70), lower=-np.ones(70), upper=np.ones(70))
     elif shape == "long_rows":
         # rows of 300 / 1100 / 2600 nonzeros span 2..11 chunks; one dense column
@@ -161,8 +162,9 @@ def test_edge_shapes_bit_exact(shape):
             vals += [1.0, -1.0]
         a = P.SparseMatrix.from_coo(rows, cols, vals, (60, n))
         dense = a.to_dense()
-        prob = P.LpProblem.from_dense(dense[:30], rng.uniform(-1, 1, 30), dense[30:],
-                                      rng.uniform(-1, 0, 30), rng.uniform(0, 1, n),
+        x0 = rng.uniform(0.5, 1.5, n)
+        prob = P.LpProblem.from_dense(dense[:30], dense[:30] @ x0, dense[30:],
+                                      dense[30:] @ x0 - 0.2, rng.uniform(0, 1, n),
                                       lower=np.zeros(n), upper=np.full(n, 3.0))
     else:
         prob = one_d_problem()
@@ -179,8 +181,9 @@ def test_edge_shapes_bit_exact(shape):
         O.iterate_once(st, slp)
     assert np.array_equal(dev.to_host("y"), st.y)
     assert np.array_equal(dev.to_host("x"), st.x)
-    rep = P.solve(prob, P.SolverConfig(tolerance=1e-6, max_iterations=3000))
-    ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(tolerance=1e-6, max_iterations=3000))
+    rep = P.solve(prob, P.SolverConfig(tolerance=1e-6, max_iterations=20000))
+    ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(tolerance=1e-6, max_iterations=20000))
+    assert ref["status"] == "Optimal"
     assert rep.status.value == ref["status"] and rep.iterations == ref["iterations"]
     assert _close(rep.primal_objective, ref["primal_objective"])
 
