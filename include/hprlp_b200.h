@@ -202,6 +202,65 @@ int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
  * measured with CUDA events on the context stream. */
 int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);
 
+/* ------------------------------------------------------------------------
+ * Row-block partitioned mode (paper_2408_12179_b200/csrc/
+ * hpr_rowblock.cuh).  Replaces the same reference steps as the single-context
+ * calls above (driver.py:293-391) for an A split by rows across P ranks.
+ *
+ * Each rank is an ordinary hpr_ctx created for its row block: dims
+ * (m_g, n, m1_g, nnz_g) with A_g = the block's rows (all n columns), bound
+ * with buffers whose column-indexed arrays (c, lower, upper, *_s, col_scale,
+ * x, anc_x, w, xb, zb, wtmp, cand_x, cand_z) hold n_pad = P*ceil(n/P)
+ * doubles, then hpr_analyze + hpr_bind_layout as usual.  The group then takes
+ * over: scale / power / run_inner / checkpoint / restart / finalize below.
+ * Rank g owns the column slice [g*ceil(n/P), min((g+1)*ceil(n/P), n)).
+ *
+ * Transports:
+ *   nccl_id != NULL: NCCL, one local rank per process (nlocal = 1), rank0 =
+ *     this process's rank; the id comes from hpr_nccl_unique_id on rank 0 and
+ *     is broadcast by the caller (torch.distributed).  libnccl.so.2 is
+ *     resolved with dlopen (the copy already loaded by PyTorch).
+ *   nccl_id == NULL: local, all nranks ranks in this process on one device
+ *     and one stream (nlocal = nranks, rank0 = 0); collectives are kernels.
+ * ------------------------------------------------------------------------ */
+typedef struct hpr_group hpr_group;
+
+int hpr_nccl_available(void);
+int hpr_nccl_unique_id(void *id, size_t bytes);          /* bytes >= 128 */
+
+/* per-rank row-block workspace (partials, reduced slice, gathered scalars) */
+int hpr_group_ws_bytes(int64_t n, int nranks, size_t *bytes);
+
+int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *const *rb_ws,
+                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0,
+                     const void *nccl_id, size_t id_bytes);
+int hpr_group_destroy(hpr_group *g);
+int hpr_group_col_range(hpr_group *g, int local, int64_t *j0, int64_t *j1);
+
+/* scale_problem (scaling.py:72-125): Ruiz column maxima all-reduced (MAX),
+ * Pock-Chambolle column sums all-reduced (SUM), norms summed over ranks. */
+int hpr_group_scale(hpr_group *g, int ruiz_iters, int pock_chambolle, int bc_normalize,
+                    hpr_scale_out *out);
+/* power_method_lambda_max (sparse.py:165-203): A^T v reduce-scatter + all-gather. */
+int hpr_group_power(hpr_group *g, double tol, int max_iters, hpr_power_out *out);
+int hpr_group_state_reset(hpr_group *g);
+/* run_inner (core.py:177-179): per iteration A_g^T y_g partial -> reduce-scatter
+ * -> x-phase on the slice -> all-gather w -> local y-phase; one CUDA graph. */
+int hpr_group_run_inner(hpr_group *g, int steps, int64_t t, int64_t k, double sigma,
+                        double lamsig, int variant);
+/* checkpoint: as hpr_checkpoint; sums are reduced per rank then across ranks in
+ * rank order, so every rank receives identical scalars. */
+int hpr_group_checkpoint(hpr_group *g, double sigma, double lamsig, int term_original,
+                         int slot, hpr_ckpt_out *out);
+int hpr_group_restart(hpr_group *g);
+int hpr_group_kkt_origin(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out);
+int hpr_group_kkt(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out);
+/* final unscale + all-gather of x and z (every rank then holds full x, z and
+ * its own rows of y) + objectives on the original problem */
+int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out);
+int hpr_group_last_times(hpr_group *g, double *inner_ms, double *ckpt_ms);
+int hpr_group_launch_count(hpr_group *g, int64_t *count);
+
 #ifdef __cplusplus
 }
 #endif

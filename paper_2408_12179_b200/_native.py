@@ -108,6 +108,42 @@ _SIGS = {
     "hpr_layout_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprLayoutInfo)]),
     "hpr_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
+    # row-block partitioned mode (hpr_rowblock.cuh)
+    "hpr_nccl_available": (ctypes.c_int, []),
+    "hpr_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
+    "hpr_group_ws_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_size_t)]),
+    "hpr_group_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p),
+                                        ctypes.POINTER(ctypes.c_void_p),
+                                        ctypes.POINTER(ctypes.c_int64), ctypes.c_size_t,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_size_t]),
+    "hpr_group_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_group_col_range": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.POINTER(ctypes.c_int64)]),
+    "hpr_group_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.POINTER(HprScaleOut)]),
+    "hpr_group_power": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
+                                       ctypes.POINTER(HprPowerOut)]),
+    "hpr_group_state_reset": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_group_run_inner": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int]),
+    "hpr_group_checkpoint": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(HprCkptOut)]),
+    "hpr_group_restart": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_group_kkt_origin": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(HprCkptOut)]),
+    "hpr_group_kkt": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(HprCkptOut)]),
+    "hpr_group_finalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(HprCkptOut)]),
+    "hpr_group_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_double)]),
+    "hpr_group_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -10,6 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
+              os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
               os.path.join(ROOT, "include", "hprlp_b200.h")]
 OUT = os.path.join(HERE, "libhprlp_b200.so")
 
@@ -19,6 +20,7 @@ NVCC_FLAGS = [
     "-fmad=false",                 # every product/sum rounded separately, like numpy/scipy
     "-Xcompiler", "-fPIC", "-shared",
     "-diag-suppress", "177", "-Xcompiler", "-Wno-deprecated-declarations",
+    "-ldl",
 ]
 
 

@@ -51,7 +51,8 @@ constexpr int kSumsqBlocks = 1024;
 // result slots of the final reduction (see hpr_ckpt_out)
 enum {
   R_BAR_DX2, R_DX2, R_DY2, R_BAR_DY2, R_PRIM2, R_BY, R_R1, R_DUAL2, R_CX, R_LZ, R_UZ, R_NLO,
-  R_NUP, R_CLAMP, R_R2, R_SH2, R_ATY2, R_SUMSQ0, R_SUMSQ1, R_SUMSQ2, R_SUMSQ3, R_POW_U2, R_COUNT
+  R_NUP, R_CLAMP, R_R2, R_SH2, R_ATY2, R_SUMSQ0, R_SUMSQ1, R_SUMSQ2, R_SUMSQ3, R_POW_U2, R_NONFIN, R_POW_VW,
+  R_POW_WW, R_COUNT
 };
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -960,3 +961,5 @@ int hpr_last_times(hpr_ctx *c, double *inner_ms, double *ckpt_ms) {
 }
 
 }  // extern "C"
+
+#include "hpr_rowblock.cuh"

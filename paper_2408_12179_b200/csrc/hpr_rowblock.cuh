@@ -1,0 +1,1081 @@
+// hpr_rowblock.cuh -- row-block partitioned HPR-LP across ranks.
+//
+// Included at the end of hpr_capi.cu (same translation unit: it reuses the
+// context internals).  A group is P ranks; rank g owns a contiguous block R_g
+// of the stacked rows of A (balanced by nonzeros), i.e. an ordinary hpr_ctx
+// whose dims are (m_g, n, m1_g, nnz_g): A_g is m_g x n and its transpose A_g^T
+// is n x m_g.  Everything row-indexed (y, b, anchors, row scale) is local.
+// Column-indexed vectors are allocated at length n_pad = P * cnt on every rank
+// (cnt = ceil(n / P)); rank g owns the column slice [g*cnt, min((g+1)*cnt, n)).
+//
+// One inner iteration (core.py:168-172):
+//   p_g   = A_g^T y_g                        SELL kernel, n partial outputs
+//   aty   = reduce-scatter(sum_g p_g)        rank g receives its cnt columns
+//   x, w  = x-phase epilogue on the slice    (EpiXIter over the slice)
+//   w     = all-gather(w slices)             every rank needs all of w
+//   y_g   = y-phase on A_g w                 local SELL kernel (EpiYIter)
+// i.e. the north star's all-reduce of the A^T y partials, split as RS + AG so
+// the n-length elementwise work is done once, not P times.  Checkpoint sums
+// (KKT, merit, sigma) are per-rank fixed-order partials, then all-gathered and
+// summed in rank order, so every rank makes the same host decisions.
+//
+// Two transports behind one interface:
+//   * NCCL (one rank per process, one GPU each; ncclReduceScatter /
+//     ncclAllGather / ncclAllReduce captured in the inner-loop CUDA graph);
+//     libnccl is resolved with dlopen at group creation (the copy PyTorch
+//     already loaded), so the library itself has no link-time NCCL dependency.
+//   * local (all P ranks in this process on ONE device and ONE stream): the
+//     collectives are small kernels over the P ranks' buffers.  This runs the
+//     partitioned algorithm bit-for-bit as P GPUs would except for the order of
+//     the cross-rank sums (rank order here; NCCL's ring order there), and is how
+//     the partitioned path is parity-tested on a single GPU.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace hpr {
+
+constexpr int kMaxLocal = 8;
+
+struct PtrSet {
+  double *p[kMaxLocal];
+};
+
+// x-phase partial of A_g^T v (row-block mode): out[j] = s
+struct EpiStore {
+  static constexpr int NQ = 0;
+  double *out;
+  const PowState *S;   // optional gate (power method)
+  __device__ bool enter() { return S == nullptr || !S->done; }
+  __device__ void prefetch(int) {}
+  __device__ void finish(int j, double s, double *) { out[j] = s; }
+};
+
+// column epilogue over a slice: epi.finish(j, s[j - j0]) for j in [j0, j1)
+template <class Epi>
+__global__ void __launch_bounds__(kThreads)
+k_cols(int j0, int j1, const double *__restrict__ s, Epi epi, double *part) {
+  double acc[Epi::NQ > 0 ? Epi::NQ : 1];
+#pragma unroll
+  for (int q = 0; q < (Epi::NQ > 0 ? Epi::NQ : 1); ++q) acc[q] = 0.0;
+  if (!epi.enter()) return;
+  for (int j = j0 + blockIdx.x * kThreads + threadIdx.x; j < j1; j += gridDim.x * kThreads) {
+    epi.prefetch(j);
+    epi.finish(j, s[j - j0], acc);
+  }
+  if constexpr (Epi::NQ > 0) block_reduce_store<Epi::NQ>(acc, part, gridDim.x);
+}
+
+// power-method u^2 over a slice (sparse.py:178 check), one partial per CTA
+__global__ void __launch_bounds__(kThreads) k_slice_sumsq(const double *s, int cnt, double *part) {
+  double acc[1] = {0.0};
+  for (int j = blockIdx.x * kThreads + threadIdx.x; j < cnt; j += gridDim.x * kThreads)
+    acc[0] = __dadd_rn(acc[0], sq(s[j]));
+  block_reduce_store<1>(acc, part, gridDim.x);
+}
+
+// ---- local transport: all ranks' buffers on one device ----------------------
+// out_g[j] = sum_{r = 0..P-1} part_r[g*cnt + j]   (rank order)
+__global__ void k_rs_local(PtrSet part, PtrSet out, int P, int cnt) {
+  const long long total = (long long)P * cnt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < P; ++r) s = __dadd_rn(s, part.p[r][e]);
+    out.p[e / cnt][e % cnt] = s;
+  }
+}
+// all-gather: vec_r[g*cnt + j] = src_g[j] for every r (src may alias vec_g + g*cnt)
+__global__ void k_ag_local(PtrSet src, PtrSet vec, int P, int cnt) {
+  const long long total = (long long)P * cnt;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(e / cnt);
+    const double v = src.p[g][e % cnt];
+    for (int r = 0; r < P; ++r)
+      if (vec.p[r] + e != src.p[g] + e % cnt) vec.p[r][e] = v;
+  }
+}
+// all-reduce in place over n entries (op 0 = sum in rank order, 2 = max)
+__global__ void k_ar_local(PtrSet v, int P, int n, int op) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double s = v.p[0][j];
+    for (int r = 1; r < P; ++r) s = op == 2 ? fmax(s, v.p[r][j]) : __dadd_rn(s, v.p[r][j]);
+    for (int r = 0; r < P; ++r) v.p[r][j] = s;
+  }
+}
+// checkpoint scalars: res_r[q] = sum over ranks in rank order; slot nonfin = min
+__global__ void k_scal_local(PtrSet res, int P, int nq, int nonfin) {
+  const int q = threadIdx.x;
+  if (q >= nq) return;
+  double s = res.p[0][q];
+  for (int r = 1; r < P; ++r) s = q == nonfin ? fmin(s, res.p[r][q]) : __dadd_rn(s, res.p[r][q]);
+  for (int r = 0; r < P; ++r) res.p[r][q] = s;
+}
+// NCCL transport: gath = P x 64 all-gathered results -> res (rank order)
+__global__ void k_scal_gathered(const double *gath, int P, int nq, int nonfin, double *res) {
+  const int q = threadIdx.x;
+  if (q >= nq) return;
+  double s = gath[q];
+  for (int r = 1; r < P; ++r) s = q == nonfin ? fmin(s, gath[r * 64 + q]) : __dadd_rn(s, gath[r * 64 + q]);
+  res[q] = s;
+}
+// first non-finite k as a double (1e300 = none) so it rides the scalar reduction
+__global__ void k_nonfin_to_result(const IterParams *P, double *slot) {
+  *slot = P->nonfinite_k == ~0ULL ? 1e300 : (double)P->nonfinite_k;
+}
+// power-method start vector: basis vector e_fb (global row fb) or ones
+__global__ void k_basis(double *v, int m, int local_row) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    v[i] = i == local_row ? 1.0 : 0.0;
+}
+
+}  // namespace hpr
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+struct NcclApi {
+  void *h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclReduceScatter) reduceScatter = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+  bool ok = false;
+};
+
+NcclApi &nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    // prefer the copy already in the process (PyTorch's), else the loader's
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.h = h;
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.reduceScatter = (decltype(api.reduceScatter))dlsym(h, "ncclReduceScatter");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce &&
+               api.reduceScatter && api.allGather && api.errStr;
+    }
+  }
+  return api;
+}
+
+#define NK(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(HPR_ENCCL, std::string(#call) + ": " + nccl().errStr(r_));               \
+  } while (0)
+
+// per-rank buffers of the row-block mode (carved from the caller's rb workspace)
+struct RbRank {
+  hpr_ctx *c = nullptr;
+  double *xpart = nullptr;   // n_pad: partial A_g^T v
+  double *xslice = nullptr;  // cnt: reduced slice
+  double *gath = nullptr;    // P * 64: all-gathered scalars (NCCL transport)
+  int64_t row0 = 0;          // first global row
+};
+
+size_t rb_layout(int64_t n, int P, size_t *o_xpart, size_t *o_xslice, size_t *o_gath) {
+  const int64_t cnt = (n + P - 1) / P;
+  size_t off = 0;
+  *o_xpart = off;
+  off = align_up(off + sizeof(double) * cnt * P, 256);
+  *o_xslice = off;
+  off = align_up(off + sizeof(double) * std::max<int64_t>(cnt, 1), 256);
+  *o_gath = off;
+  off = align_up(off + sizeof(double) * 64 * P, 256);
+  return off;
+}
+
+}  // namespace
+
+struct hpr_group {
+  int P = 1;          // ranks in the group
+  int rank0 = 0;      // global rank of local rank 0
+  int nlocal = 1;
+  int64_t n = 0, cnt = 0;
+  std::vector<RbRank> r;
+  ncclComm_t comm = nullptr;
+  bool use_nccl = false;
+  cudaStream_t stream = nullptr;   // ctx[0]'s stream (local transport: shared)
+  std::map<int, cudaGraphExec_t> inner_graphs;
+  cudaGraphExec_t pow_graph = nullptr;
+  bool inner_timed = false, ckpt_timed = false;
+
+  int j0(int l) const { return (int)std::min<int64_t>((int64_t)(rank0 + l) * cnt, n); }
+  int j1(int l) const { return (int)std::min<int64_t>((int64_t)(rank0 + l + 1) * cnt, n); }
+};
+
+namespace {
+
+PtrSet ptrs(hpr_group *g, double *RbRank::*f) {
+  PtrSet s{};
+  for (int l = 0; l < g->nlocal; ++l) s.p[l] = g->r[l].*f;
+  return s;
+}
+
+// sum of xpart over ranks -> xslice of each rank
+int g_reduce_scatter(hpr_group *g) {
+  if (g->P == 1 && !g->use_nccl) {
+    CK(cudaMemcpyAsync(g->r[0].xslice, g->r[0].xpart, sizeof(double) * g->cnt,
+                       cudaMemcpyDeviceToDevice, g->stream));
+    return HPR_OK;
+  }
+  if (g->use_nccl) {
+    NK(nccl().reduceScatter(g->r[0].xpart, g->r[0].xslice, (size_t)g->cnt, ncclFloat64, ncclSum,
+                            g->comm, g->r[0].c->stream));
+    return HPR_OK;
+  }
+  const long long total = (long long)g->P * g->cnt;
+  k_rs_local<<<grid_for(total), 256, 0, g->stream>>>(ptrs(g, &RbRank::xpart), ptrs(g, &RbRank::xslice),
+                                                     g->P, (int)g->cnt);
+  CKL();
+  g->r[0].c->launches += 1;
+  return HPR_OK;
+}
+
+// every rank's full vector vec(l) <- concatenation of the ranks' slices.  src(l)
+// is the slice owned by local rank l (may alias vec(l) + j0(l)).
+template <class VecOf, class SrcOf>
+int g_all_gather(hpr_group *g, VecOf vec, SrcOf src) {
+  if (g->P == 1 && !g->use_nccl) {
+    const double *s = src(0);
+    double *v = vec(0);
+    if (s != v) CK(cudaMemcpyAsync(v, s, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, g->stream));
+    return HPR_OK;
+  }
+  if (g->use_nccl) {
+    NK(nccl().allGather(src(0), vec(0), (size_t)g->cnt, ncclFloat64, g->comm, g->r[0].c->stream));
+    return HPR_OK;
+  }
+  PtrSet ps{}, pv{};
+  for (int l = 0; l < g->nlocal; ++l) {
+    ps.p[l] = const_cast<double *>(src(l));
+    pv.p[l] = vec(l);
+  }
+  const long long total = (long long)g->P * g->cnt;
+  k_ag_local<<<grid_for(total), 256, 0, g->stream>>>(ps, pv, g->P, (int)g->cnt);
+  CKL();
+  g->r[0].c->launches += 1;
+  return HPR_OK;
+}
+
+// in-place all-reduce of an n-vector (Ruiz column max / PC column sums)
+template <class VecOf>
+int g_all_reduce(hpr_group *g, VecOf vec, int64_t count, bool is_max) {
+  if (g->P == 1 && !g->use_nccl) return HPR_OK;
+  if (g->use_nccl) {
+    NK(nccl().allReduce(vec(0), vec(0), (size_t)count, ncclFloat64, is_max ? ncclMax : ncclSum,
+                        g->comm, g->r[0].c->stream));
+    return HPR_OK;
+  }
+  PtrSet pv{};
+  for (int l = 0; l < g->nlocal; ++l) pv.p[l] = vec(l);
+  k_ar_local<<<grid_for(count), 256, 0, g->stream>>>(pv, g->P, (int)count, is_max ? 2 : 0);
+  CKL();
+  g->r[0].c->launches += 1;
+  return HPR_OK;
+}
+
+// group sum of every rank's results[0..R_COUNT) (rank order), min for R_NONFIN
+int g_scalars(hpr_group *g) {
+  if (g->P == 1 && !g->use_nccl) return HPR_OK;
+  if (g->use_nccl) {
+    hpr_ctx *c = g->r[0].c;
+    NK(nccl().allGather(c->results, g->r[0].gath, 64, ncclFloat64, g->comm, c->stream));
+    k_scal_gathered<<<1, 64, 0, c->stream>>>(g->r[0].gath, g->P, R_COUNT, R_NONFIN, c->results);
+    CKL();
+    c->launches += 1;
+    return HPR_OK;
+  }
+  PtrSet pr{};
+  for (int l = 0; l < g->nlocal; ++l) pr.p[l] = g->r[l].c->results;
+  k_scal_local<<<1, 64, 0, g->stream>>>(pr, g->P, R_COUNT, R_NONFIN);
+  CKL();
+  g->r[0].c->launches += 1;
+  return HPR_OK;
+}
+
+int g_fetch(hpr_group *g) {
+  // every rank holds the same reduced scalars; read local rank 0's
+  return fetch_results(g->r[0].c);
+}
+
+// SELL launch of A_l^T with the store epilogue into xpart (over all n rows)
+int g_at_partial(hpr_group *g, int l, bool scaled, const double *v, const PowState *gate) {
+  hpr_ctx *c = g->r[l].c;
+  EpiStore es{};
+  es.out = g->r[l].xpart;
+  es.S = gate;
+  return launch_sell(c, c->mat_at(scaled), v, es, nullptr, nullptr);
+}
+
+template <class Epi>
+int g_cols(hpr_group *g, int l, const Epi &epi, double *part, int *grid_out) {
+  hpr_ctx *c = g->r[l].c;
+  const int j0 = g->j0(l), j1 = g->j1(l);
+  const int grid = std::max(1, std::min(grid_for(std::max(j1 - j0, 1), kThreads), c->num_sms * 4));
+  k_cols<Epi><<<grid, kThreads, 0, c->stream>>>(j0, j1, g->r[l].xslice, epi, part);
+  CKL();
+  c->launches += 1;
+  if (grid_out) *grid_out = grid;
+  return HPR_OK;
+}
+
+int g_check(hpr_group *g) {
+  if (!g) return fail(HPR_EINVAL, "null group");
+  for (auto &rr : g->r) {
+    int rc = check_ctx(rr.c, true, false);
+    if (rc) return rc;
+  }
+  return HPR_OK;
+}
+
+int g_check_scaled(hpr_group *g) {
+  int rc = g_check(g);
+  if (rc) return rc;
+  for (auto &rr : g->r)
+    if (!rr.c->scaled) return fail(HPR_ESTATE, "hpr_group_scale has not been called");
+  return HPR_OK;
+}
+
+// KKT terms of candidate `slot` on every rank: rows local, columns on the slice
+int g_kkt(hpr_group *g, int term_original, int slot, std::vector<std::vector<RedSeg>> &segs) {
+  for (int l = 0; l < g->nlocal; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    int rc = g_at_partial(g, l, !term_original, c->B.cand_y[slot], nullptr);
+    if (rc) return rc;
+  }
+  int rc = g_reduce_scatter(g);
+  if (rc) return rc;
+  for (int l = 0; l < g->nlocal; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    const hpr_buffers &B = c->B;
+    Parts P = parts_of(c);
+    EpiKktRow er{};
+    er.b = term_original ? B.b : B.b_s;
+    er.cy = B.cand_y[slot];
+    er.m1 = (int)c->d.m1;
+    int ga = 0, gat = 0;
+    rc = launch_sell(c, c->mat_a(!term_original), B.cand_x[slot], er, P.krow, &ga);
+    if (rc) return rc;
+    EpiKktCol ec{};
+    ec.c = term_original ? B.c : B.c_s;
+    ec.lo = term_original ? B.lower : B.lower_s;
+    ec.up = term_original ? B.upper : B.upper_s;
+    ec.cx = B.cand_x[slot];
+    ec.cz = B.cand_z[slot];
+    rc = g_cols(g, l, ec, P.kcol, &gat);
+    if (rc) return rc;
+    auto &sg = segs[l];
+    sg.push_back({P.krow + 0 * ga, ga, R_PRIM2});
+    sg.push_back({P.krow + 1 * ga, ga, R_BY});
+    sg.push_back({P.krow + 2 * ga, ga, R_R1});
+    const int outs[8] = {R_DUAL2, R_CX, R_LZ, R_UZ, R_NLO, R_NUP, R_CLAMP, R_R2};
+    for (int q = 0; q < 8; ++q) sg.push_back({P.kcol + q * gat, gat, outs[q]});
+  }
+  return HPR_OK;
+}
+
+int g_reduce_all(hpr_group *g, std::vector<std::vector<RedSeg>> &segs, bool with_nonfin) {
+  for (int l = 0; l < g->nlocal; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, c->stream));
+    if (!segs[l].empty()) {
+      int rc = reduce_final(c, segs[l]);
+      if (rc) return rc;
+    }
+    if (with_nonfin) {
+      k_nonfin_to_result<<<1, 1, 0, c->stream>>>(c->params, c->results + R_NONFIN);
+      CKL();
+      c->launches += 1;
+    } else {
+      k_fill<<<1, 32, 0, c->stream>>>(c->results + R_NONFIN, 1e300, 1);
+      CKL();
+      c->launches += 1;
+    }
+  }
+  return g_scalars(g);
+}
+
+void g_fill_out(hpr_group *g, hpr_ckpt_out *o) {
+  fill_out(g->r[0].c, o);
+  const double nf = g->r[0].c->h_results[R_NONFIN];
+  o->nonfinite_k = nf >= 1e299 ? -1 : (int64_t)nf;
+}
+
+int g_kkt_common(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out) {
+  std::vector<std::vector<RedSeg>> segs(g->nlocal);
+  int rc = g_kkt(g, term_original, slot, segs);
+  if (rc) return rc;
+  rc = g_reduce_all(g, segs, false);
+  if (rc) return rc;
+  rc = g_fetch(g);
+  if (rc) return rc;
+  g_fill_out(g, out);
+  return HPR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpr_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+int hpr_nccl_unique_id(void *id, size_t bytes) {
+  if (!id || bytes < sizeof(ncclUniqueId)) return fail(HPR_EINVAL, "id buffer too small");
+  if (!nccl().ok) return fail(HPR_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId u;
+  NK(nccl().getUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return HPR_OK;
+}
+
+int hpr_group_ws_bytes(int64_t n, int nranks, size_t *bytes) {
+  if (!bytes || n < 1 || nranks < 1) return fail(HPR_EINVAL, "bad argument");
+  size_t a, b, c;
+  *bytes = rb_layout(n, nranks, &a, &b, &c);
+  return HPR_OK;
+}
+
+int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *const *rb_ws,
+                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0,
+                     const void *nccl_id, size_t id_bytes) {
+  if (!out || !ctxs || !rb_ws || !row0 || nlocal < 1 || nranks < 1)
+    return fail(HPR_EINVAL, "bad argument");
+  if (nlocal > kMaxLocal) return fail(HPR_EINVAL, "too many local ranks");
+  const bool use_nccl = nccl_id != nullptr;
+  if (use_nccl && nlocal != 1) return fail(HPR_EINVAL, "NCCL transport: one local rank per process");
+  if (!use_nccl && (nlocal != nranks || rank0 != 0))
+    return fail(HPR_EINVAL, "local transport: all ranks must be local");
+  const int64_t n = ctxs[0]->d.n;
+  size_t o_xpart, o_xslice, o_gath;
+  const size_t need = rb_layout(n, nranks, &o_xpart, &o_xslice, &o_gath);
+  if (rb_ws_bytes < need) return fail(HPR_EINVAL, "row-block workspace too small");
+  for (int l = 0; l < nlocal; ++l) {
+    if (!ctxs[l] || !rb_ws[l]) return fail(HPR_EINVAL, "null context or workspace");
+    if (ctxs[l]->d.n != n) return fail(HPR_EINVAL, "ranks disagree on n");
+    if (!use_nccl && (ctxs[l]->stream != ctxs[0]->stream || ctxs[l]->device != ctxs[0]->device))
+      return fail(HPR_EINVAL, "local transport: ranks must share one device and stream");
+  }
+  hpr_group *g = new hpr_group();
+  g->P = nranks;
+  g->rank0 = rank0;
+  g->nlocal = nlocal;
+  g->n = n;
+  g->cnt = (n + nranks - 1) / nranks;
+  g->stream = ctxs[0]->stream;
+  g->use_nccl = use_nccl;
+  for (int l = 0; l < nlocal; ++l) {
+    RbRank rr;
+    rr.c = ctxs[l];
+    char *w = (char *)rb_ws[l];
+    rr.xpart = (double *)(w + o_xpart);
+    rr.xslice = (double *)(w + o_xslice);
+    rr.gath = (double *)(w + o_gath);
+    rr.row0 = row0[l];
+    g->r.push_back(rr);
+  }
+  if (g->use_nccl) {
+    if (!nccl().ok) {
+      delete g;
+      return fail(HPR_ENCCL, "libnccl.so.2 not loadable");
+    }
+    if (id_bytes < sizeof(ncclUniqueId)) {
+      delete g;
+      return fail(HPR_EINVAL, "bad NCCL id");
+    }
+    ncclUniqueId u;
+    std::memcpy(&u, nccl_id, sizeof(u));
+    cudaSetDevice(ctxs[0]->device);
+    ncclResult_t r = nccl().commInitRank(&g->comm, nranks, u, rank0);
+    if (r != ncclSuccess) {
+      delete g;
+      return fail(HPR_ENCCL, std::string("ncclCommInitRank: ") + nccl().errStr(r));
+    }
+  }
+  *out = g;
+  return HPR_OK;
+}
+
+int hpr_group_destroy(hpr_group *g) {
+  if (!g) return HPR_OK;
+  for (auto &kv : g->inner_graphs) cudaGraphExecDestroy(kv.second);
+  if (g->pow_graph) cudaGraphExecDestroy(g->pow_graph);
+  if (g->comm) nccl().commDestroy(g->comm);
+  delete g;
+  return HPR_OK;
+}
+
+int hpr_group_col_range(hpr_group *g, int local, int64_t *j0, int64_t *j1) {
+  if (!g || !j0 || !j1 || local < 0 || local >= g->nlocal) return fail(HPR_EINVAL, "bad argument");
+  *j0 = g->j0(local);
+  *j1 = g->j1(local);
+  return HPR_OK;
+}
+
+// scale_problem (scaling.py:72-125) across the row blocks: row factors are
+// local, column factors are reduced (max for Ruiz -- exact; sum for PC).
+int hpr_group_scale(hpr_group *g, int ruiz_iters, int pock_chambolle, int bc_normalize,
+                    hpr_scale_out *out) {
+  int rc = g_check(g);
+  if (rc) return rc;
+  CK(cudaSetDevice(g->r[0].c->device));
+  const int n = (int)g->n;
+  auto dcv = [&](int l) { return g->r[l].c->dvec_n; };
+  for (auto &rr : g->r) {
+    hpr_ctx *c = rr.c;
+    const hpr_buffers &B = c->B;
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(B.a_val_s, B.a_val, sizeof(double) * c->d.nnz, cudaMemcpyDeviceToDevice, s));
+    k_fill<<<grid_for(c->d.m), 256, 0, s>>>(B.row_scale, 1.0, c->d.m);
+    k_fill<<<grid_for(n), 256, 0, s>>>(B.col_scale, 1.0, n);
+    CKL();
+    c->launches += 2;
+  }
+  auto pass = [&](bool ruiz) -> int {
+    for (auto &rr : g->r) {
+      hpr_ctx *c = rr.c;
+      const hpr_buffers &B = c->B;
+      const int m = (int)c->d.m;
+      if (ruiz) {
+        k_row_maxabs<<<grid_for(m), 256, 0, c->stream>>>(B.a_rp, B.a_val_s, m, c->dvec_m);
+        k_col_maxabs<<<grid_for(n), 256, 0, c->stream>>>(B.at_rp, B.at_perm, B.a_val_s, n, c->dvec_n);
+      } else {
+        k_row_abssum<<<grid_for(m), 256, 0, c->stream>>>(B.a_rp, B.a_val_s, m, c->dvec_m);
+        k_col_abssum<<<grid_for(n), 256, 0, c->stream>>>(B.at_rp, B.at_perm, B.a_val_s, n, c->dvec_n);
+      }
+      CKL();
+      c->launches += 2;
+    }
+    int rc2 = g_all_reduce(g, dcv, n, ruiz);
+    if (rc2) return rc2;
+    for (auto &rr : g->r) {
+      hpr_ctx *c = rr.c;
+      const hpr_buffers &B = c->B;
+      const int m = (int)c->d.m;
+      k_sqrt_div<<<grid_for(m), 256, 0, c->stream>>>(c->dvec_m, B.row_scale, m);
+      k_sqrt_div<<<grid_for(n), 256, 0, c->stream>>>(c->dvec_n, B.col_scale, n);
+      k_scale_vals<<<grid_for((int64_t)m * 32), 256, 0, c->stream>>>(B.a_rp, B.a_ci, B.a_val_s,
+                                                                     c->dvec_m, c->dvec_n, m);
+      CKL();
+      c->launches += 3;
+    }
+    return HPR_OK;
+  };
+  for (int it = 0; it < ruiz_iters; ++it) {
+    rc = pass(true);
+    if (rc) return rc;
+  }
+  if (pock_chambolle) {
+    rc = pass(false);
+    if (rc) return rc;
+  }
+  for (auto &rr : g->r) {
+    hpr_ctx *c = rr.c;
+    const hpr_buffers &B = c->B;
+    const int m = (int)c->d.m;
+    k_scale_vecs<<<grid_for(std::max(m, n)), 256, 0, c->stream>>>(
+        B.b, B.row_scale, B.b_s, m, B.c, B.lower, B.upper, B.col_scale, B.c_s, B.lower_s,
+        B.upper_s, n);
+    CKL();
+    c->launches += 1;
+  }
+  // sum of squares of a row vector (local rows) and of a column vector (own slice)
+  auto sumsq_pair = [&](bool orig, int slot_b, int slot_c, std::vector<std::vector<RedSeg>> &segs,
+                        int bank) -> int {
+    for (int l = 0; l < g->nlocal; ++l) {
+      hpr_ctx *c = g->r[l].c;
+      const hpr_buffers &B = c->B;
+      Parts P = parts_of(c);
+      const int m = (int)c->d.m;
+      const int j0 = g->j0(l), cntl = g->j1(l) - j0;
+      const int nb0 = sumsq_blocks(m), nb1 = sumsq_blocks(std::max(cntl, 1));
+      double *pb = P.misc + (2 * bank) * kSumsqBlocks, *pc = P.misc + (2 * bank + 1) * kSumsqBlocks;
+      k_sumsq<<<nb0, kThreads, 0, c->stream>>>(orig ? B.b : B.b_s, m, pb);
+      k_sumsq<<<nb1, kThreads, 0, c->stream>>>((orig ? B.c : B.c_s) + j0, cntl, pc);
+      CKL();
+      c->launches += 2;
+      segs[l].push_back({pb, nb0, slot_b});
+      segs[l].push_back({pc, nb1, slot_c});
+    }
+    return HPR_OK;
+  };
+  if (bc_normalize) {
+    std::vector<std::vector<RedSeg>> segs(g->nlocal);
+    rc = sumsq_pair(false, R_SUMSQ0, R_SUMSQ1, segs, 0);
+    if (rc) return rc;
+    rc = g_reduce_all(g, segs, false);
+    if (rc) return rc;
+    for (auto &rr : g->r) {
+      hpr_ctx *c = rr.c;
+      const hpr_buffers &B = c->B;
+      k_factors<<<1, 32, 0, c->stream>>>(c->results + R_SUMSQ0, c->fac);
+      k_bc_normalize<<<grid_for(std::max((int)c->d.m, n)), 256, 0, c->stream>>>(
+          B.b_s, (int)c->d.m, B.c_s, B.lower_s, B.upper_s, n, c->fac);
+      CKL();
+      c->launches += 2;
+    }
+  } else {
+    for (auto &rr : g->r) {
+      k_fill<<<1, 32, 0, rr.c->stream>>>(rr.c->fac, 1.0, 2);
+      CKL();
+    }
+  }
+  for (auto &rr : g->r) {
+    hpr_ctx *c = rr.c;
+    const hpr_buffers &B = c->B;
+    const long long nnz = c->d.nnz;
+    if (nnz > 0) {
+      k_gather_vals<<<grid_for(nnz), 256, 0, c->stream>>>(B.at_perm, B.a_val_s, B.at_val_s, nnz);
+      k_sell_scatter<<<grid_for(nnz), 256, 0, c->stream>>>(c->sa.pos, B.a_val_s, c->sa.val_s, nnz);
+      k_sell_scatter<<<grid_for(nnz), 256, 0, c->stream>>>(c->sat.pos, B.at_val_s, c->sat.val_s, nnz);
+      CKL();
+      c->launches += 3;
+    }
+  }
+  std::vector<std::vector<RedSeg>> segs(g->nlocal);
+  rc = sumsq_pair(true, R_SUMSQ0, R_SUMSQ1, segs, 0);
+  if (rc) return rc;
+  rc = sumsq_pair(false, R_SUMSQ2, R_SUMSQ3, segs, 1);
+  if (rc) return rc;
+  rc = g_reduce_all(g, segs, false);
+  if (rc) return rc;
+  double fac[2];
+  CK(cudaMemcpyAsync(fac, g->r[0].c->fac, sizeof(fac), cudaMemcpyDeviceToHost, g->r[0].c->stream));
+  rc = g_fetch(g);
+  if (rc) return rc;
+  const double *h = g->r[0].c->h_results;
+  if (out) {
+    out->b_factor = fac[0];
+    out->c_factor = fac[1];
+    out->bnorm_orig = std::sqrt(h[R_SUMSQ0]);
+    out->cnorm_orig = std::sqrt(h[R_SUMSQ1]);
+    out->bnorm_s = std::sqrt(h[R_SUMSQ2]);
+    out->cnorm_s = std::sqrt(h[R_SUMSQ3]);
+  }
+  for (auto &rr : g->r) rr.c->scaled = true;
+  for (auto &kv : g->inner_graphs) cudaGraphExecDestroy(kv.second);
+  g->inner_graphs.clear();
+  return HPR_OK;
+}
+
+// power_method_lambda_max (sparse.py:165-203) over the row blocks.
+int hpr_group_power(hpr_group *g, double tol, int max_iters, hpr_power_out *out) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (!out) return fail(HPR_EINVAL, "null out");
+  CK(cudaSetDevice(g->r[0].c->device));
+  int64_t m_total = 0, nnz_total = 0;
+  for (auto &rr : g->r) {
+    m_total += rr.c->d.m;
+    nnz_total += rr.c->d.nnz;
+  }
+  if (g->use_nccl) {
+    // global row count / nnz: one tiny all-reduce through the scalar path
+    hpr_ctx *c = g->r[0].c;
+    double h[2] = {(double)m_total, (double)nnz_total};
+    CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, c->stream));
+    CK(cudaMemcpyAsync(c->results, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    k_fill<<<1, 32, 0, c->stream>>>(c->results + R_NONFIN, 1e300, 1);
+    rc = g_scalars(g);
+    if (rc) return rc;
+    rc = g_fetch(g);
+    if (rc) return rc;
+    m_total = (int64_t)c->h_results[0];
+    nnz_total = (int64_t)c->h_results[1];
+  }
+  if (nnz_total == 0) return fail(HPR_EINVAL, "matrix must be non-zero");
+  PowState st{};
+  st.tol = tol;
+  st.max_iters = max_iters;
+  auto vbuf = [&](int l) { return g->r[l].c->B.yb; };
+  auto ubuf = [&](int l) { return g->r[l].c->B.wtmp; };
+  auto wbuf = [&](int l) { return g->r[l].c->B.dy; };
+  // start vector: all ones, then basis vectors e_0, e_1, ... while A^T v == 0
+  bool found = false;
+  int64_t fb_found = -2;
+  for (int64_t fb = -1; fb < m_total && !found; ++fb) {
+    std::vector<std::vector<RedSeg>> segs(g->nlocal);
+    for (int l = 0; l < g->nlocal; ++l) {
+      hpr_ctx *c = g->r[l].c;
+      const int m = (int)c->d.m;
+      if (fb < 0) {
+        k_fill<<<grid_for(m), 256, 0, c->stream>>>(vbuf(l), 1.0, m);
+      } else {
+        const int64_t lr = fb - g->r[l].row0;
+        k_basis<<<grid_for(m), 256, 0, c->stream>>>(vbuf(l), m, (lr >= 0 && lr < m) ? (int)lr : -1);
+      }
+      CKL();
+      c->launches += 1;
+      rc = g_at_partial(g, l, true, vbuf(l), nullptr);
+      if (rc) return rc;
+    }
+    rc = g_reduce_scatter(g);
+    if (rc) return rc;
+    for (int l = 0; l < g->nlocal; ++l) {
+      hpr_ctx *c = g->r[l].c;
+      Parts P = parts_of(c);
+      const int cntl = g->j1(l) - g->j0(l);
+      const int nb = sumsq_blocks(std::max(cntl, 1));
+      k_slice_sumsq<<<nb, kThreads, 0, c->stream>>>(g->r[l].xslice, cntl, P.powt);
+      CKL();
+      c->launches += 1;
+      segs[l].push_back({P.powt, nb, R_POW_U2});
+    }
+    rc = g_reduce_all(g, segs, false);
+    if (rc) return rc;
+    rc = g_fetch(g);
+    if (rc) return rc;
+    if (std::sqrt(g->r[0].c->h_results[R_POW_U2]) > 0.0) {
+      found = true;
+      fb_found = fb;
+    }
+  }
+  if (!found) return fail(HPR_EINVAL, "A^T v = 0 for every start vector");
+  if (fb_found == -1) {
+    const double inv = 1.0 / std::sqrt((double)m_total);
+    for (int l = 0; l < g->nlocal; ++l) {
+      hpr_ctx *c = g->r[l].c;
+      k_fill<<<grid_for(c->d.m), 256, 0, c->stream>>>(vbuf(l), inv, c->d.m);
+      CKL();
+      c->launches += 1;
+    }
+  }
+  for (auto &rr : g->r)
+    CK(cudaMemcpyAsync(rr.c->pow, &st, sizeof(st), cudaMemcpyHostToDevice, rr.c->stream));
+  if (max_iters <= 0) {
+    out->value = out->raw = 0.0;
+    out->iterations = out->converged = 0;
+    return HPR_OK;
+  }
+  if (!g->pow_graph) {
+    cudaGraph_t gr;
+    std::vector<long long> before;
+    for (auto &rr : g->r) before.push_back(rr.c->launches);
+    CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kPowBatch && !rc; ++i) {
+      std::vector<std::vector<RedSeg>> segs(g->nlocal);
+      // u = A^T v: partial -> reduce-scatter -> all-gather
+      for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, vbuf(l), g->r[l].c->pow);
+      if (!rc) rc = g_reduce_scatter(g);
+      if (!rc)
+        rc = g_all_gather(g, ubuf, [&](int l) -> const double * { return g->r[l].xslice; });
+      // w = A_g u, local sums v.w and w.w
+      for (int l = 0; l < g->nlocal && !rc; ++l) {
+        hpr_ctx *c = g->r[l].c;
+        Parts P = parts_of(c);
+        EpiPowA ea{};
+        ea.v = vbuf(l);
+        ea.wv = wbuf(l);
+        ea.S = c->pow;
+        int ga = 0;
+        rc = launch_sell(c, c->mat_a(true), ubuf(l), ea, P.powa, &ga);
+        segs[l].push_back({P.powa, ga, R_POW_VW});
+        segs[l].push_back({P.powa + ga, ga, R_POW_WW});
+      }
+      if (!rc) rc = g_reduce_all(g, segs, false);
+      for (int l = 0; l < g->nlocal && !rc; ++l) {
+        hpr_ctx *c = g->r[l].c;
+        k_pow_step<<<1, kThreads, 0, c->stream>>>(c->results + R_POW_VW, 1, c->pow);
+        k_pow_norm<<<grid_for(c->d.m), 256, 0, c->stream>>>(wbuf(l), vbuf(l), (int)c->d.m, c->pow);
+        k_pow_norm_done<<<1, 1, 0, c->stream>>>(c->pow);
+        c->launches += 3;
+      }
+    }
+    cudaError_t e = cudaStreamEndCapture(g->stream, &gr);
+    if (rc) {
+      if (e == cudaSuccess) cudaGraphDestroy(gr);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("pow capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&g->pow_graph, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("pow instantiate: ") + cudaGetErrorString(e));
+    for (int l = 0; l < g->nlocal; ++l) g->r[l].c->launches = before[l];
+  }
+  hpr_ctx *c0 = g->r[0].c;
+  for (;;) {
+    CK(cudaGraphLaunch(g->pow_graph, g->stream));
+    c0->launches += (long long)kPowBatch * (6 * g->nlocal + 1);
+    CK(cudaMemcpyAsync(c0->h_pow, c0->pow, sizeof(PowState), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (c0->h_pow->done) break;
+  }
+  out->raw = c0->h_pow->lam;
+  out->value = c0->h_pow->lam * (1.0 + 1e-3);
+  out->iterations = c0->h_pow->iters;
+  out->converged = c0->h_pow->converged;
+  return HPR_OK;
+}
+
+int hpr_group_state_reset(hpr_group *g) {
+  int rc = g_check(g);
+  if (rc) return rc;
+  for (auto &rr : g->r) {
+    rc = hpr_state_reset(rr.c);
+    if (rc) return rc;
+  }
+  return HPR_OK;
+}
+
+// run_inner (core.py:177-179) over the row blocks, one CUDA graph per `steps`.
+int hpr_group_run_inner(hpr_group *g, int steps, int64_t t, int64_t k, double sigma,
+                        double lamsig, int variant) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (steps <= 0) return HPR_OK;
+  if (variant < 0 || variant > 2) return fail(HPR_EINVAL, "bad variant");
+  CK(cudaSetDevice(g->r[0].c->device));
+  auto it = g->inner_graphs.find(steps);
+  if (it == g->inner_graphs.end()) {
+    std::vector<long long> before;
+    for (auto &rr : g->r) before.push_back(rr.c->launches);
+    cudaGraph_t gr;
+    CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+    auto wvec = [&](int l) { return g->r[l].c->B.w; };
+    auto wsl = [&](int l) -> const double * { return g->r[l].c->B.w + g->j0(l); };
+    for (int i = 0; i < steps && !rc; ++i) {
+      for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, g->r[l].c->B.y, nullptr);
+      if (!rc) rc = g_reduce_scatter(g);
+      for (int l = 0; l < g->nlocal && !rc; ++l) {
+        hpr_ctx *c = g->r[l].c;
+        const hpr_buffers &B = c->B;
+        EpiXIter ex{};
+        ex.c = B.c_s;
+        ex.lo = B.lower_s;
+        ex.up = B.upper_s;
+        ex.anc = B.anc_x;
+        ex.x = B.x;
+        ex.w = B.w;
+        ex.P = c->params;
+        ex.step = i;
+        rc = g_cols(g, l, ex, nullptr, nullptr);
+      }
+      if (!rc) rc = g_all_gather(g, wvec, wsl);
+      for (int l = 0; l < g->nlocal && !rc; ++l) {
+        hpr_ctx *c = g->r[l].c;
+        const hpr_buffers &B = c->B;
+        EpiYIter ey{};
+        ey.b = B.b_s;
+        ey.anc = B.anc_y;
+        ey.y = B.y;
+        ey.P = c->params;
+        ey.m1 = (int)c->d.m1;
+        ey.step = i;
+        rc = launch_sell(c, c->mat_a(true), B.w, ey, nullptr, nullptr);
+      }
+    }
+    cudaError_t e = cudaStreamEndCapture(g->stream, &gr);
+    if (rc) {
+      if (e == cudaSuccess) cudaGraphDestroy(gr);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exe;
+    e = cudaGraphInstantiate(&exe, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    for (int l = 0; l < g->nlocal; ++l) g->r[l].c->launches = before[l];
+    it = g->inner_graphs.emplace(steps, exe).first;
+  }
+  for (auto &rr : g->r) {
+    k_set_params<<<1, 1, 0, rr.c->stream>>>(rr.c->params, sigma, lamsig, (long long)t, (long long)k,
+                                            variant);
+    CKL();
+  }
+  hpr_ctx *c0 = g->r[0].c;
+  CK(cudaEventRecord(c0->ev0, g->stream));
+  CK(cudaGraphLaunch(it->second, g->stream));
+  CK(cudaEventRecord(c0->ev1, g->stream));
+  g->inner_timed = true;
+  c0->inner_timed = true;
+  // per step: nlocal x (A^T partial + slice epilogue + y phase) + the collectives
+  const int coll = (g->P == 1 || g->use_nccl) ? 0 : 2;
+  c0->launches += g->nlocal + (long long)steps * (3 * g->nlocal + coll);
+  return HPR_OK;
+}
+
+// checkpoint (driver.py:329-339 + core.py:118-129, 182-218) over the row blocks
+int hpr_group_checkpoint(hpr_group *g, double sigma, double lamsig, int term_original, int slot,
+                         hpr_ckpt_out *out) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
+  CK(cudaSetDevice(g->r[0].c->device));
+  hpr_ctx *c0 = g->r[0].c;
+  CK(cudaEventRecord(c0->ev2, g->stream));
+  std::vector<std::vector<RedSeg>> segs(g->nlocal);
+  // half step, x part: A^T y partial -> RS -> slice epilogue
+  for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, g->r[l].c->B.y, nullptr);
+  if (!rc) rc = g_reduce_scatter(g);
+  for (int l = 0; l < g->nlocal && !rc; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    const hpr_buffers &B = c->B;
+    Parts P = parts_of(c);
+    CandCtx cc{term_original, c->fac, B.row_scale, B.col_scale, B.lower, B.upper};
+    EpiXHalf ex{};
+    ex.x = B.x;
+    ex.c = B.c_s;
+    ex.lo = B.lower_s;
+    ex.up = B.upper_s;
+    ex.anc = B.anc_x;
+    ex.xb_out = B.xb;
+    ex.zb_out = B.zb;
+    ex.wtmp = B.wtmp;
+    ex.cx_out = B.cand_x[slot];
+    ex.cz_out = B.cand_z[slot];
+    ex.cc = cc;
+    ex.sigma = sigma;
+    int gx = 0;
+    rc = g_cols(g, l, ex, P.xhalf, &gx);
+    segs[l].push_back({P.xhalf, gx, R_BAR_DX2});
+    segs[l].push_back({P.xhalf + gx, gx, R_DX2});
+  }
+  if (rc) return rc;
+  // the y phase and the row KKT terms gather wtmp and cand_x over all columns
+  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.wtmp; },
+                    [&](int l) -> const double * { return g->r[l].c->B.wtmp + g->j0(l); });
+  if (!rc)
+    rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[slot]; },
+                      [&](int l) -> const double * { return g->r[l].c->B.cand_x[slot] + g->j0(l); });
+  for (int l = 0; l < g->nlocal && !rc; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    const hpr_buffers &B = c->B;
+    Parts P = parts_of(c);
+    CandCtx cc{term_original, c->fac, B.row_scale, B.col_scale, B.lower, B.upper};
+    EpiYHalf ey{};
+    ey.y = B.y;
+    ey.b = B.b_s;
+    ey.anc = B.anc_y;
+    ey.yb_out = B.yb;
+    ey.dy_out = B.dy;
+    ey.cy_out = B.cand_y[slot];
+    ey.cc = cc;
+    ey.lamsig = lamsig;
+    ey.m1 = (int)c->d.m1;
+    int gy = 0;
+    rc = launch_sell(c, c->mat_a(true), B.wtmp, ey, P.yhalf, &gy);
+    segs[l].push_back({P.yhalf, gy, R_DY2});
+    segs[l].push_back({P.yhalf + gy, gy, R_BAR_DY2});
+  }
+  // merit: A^T dy partial -> RS -> slice epilogue
+  for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, g->r[l].c->B.dy, nullptr);
+  if (!rc) rc = g_reduce_scatter(g);
+  for (int l = 0; l < g->nlocal && !rc; ++l) {
+    hpr_ctx *c = g->r[l].c;
+    Parts P = parts_of(c);
+    EpiMeritCol em{};
+    em.x = c->B.x;
+    em.xb = c->B.xb;
+    em.sigma = sigma;
+    int gm = 0;
+    rc = g_cols(g, l, em, P.merit, &gm);
+    segs[l].push_back({P.merit, gm, R_SH2});
+    segs[l].push_back({P.merit + gm, gm, R_ATY2});
+  }
+  if (!rc) rc = g_kkt(g, term_original, slot, segs);
+  if (!rc) rc = g_reduce_all(g, segs, true);
+  if (rc) return rc;
+  CK(cudaEventRecord(c0->ev3, g->stream));
+  rc = g_fetch(g);
+  if (rc) return rc;
+  c0->ckpt_timed = true;
+  g->ckpt_timed = true;
+  g_fill_out(g, out);
+  return HPR_OK;
+}
+
+int hpr_group_restart(hpr_group *g) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  for (auto &rr : g->r) {
+    rc = hpr_restart(rr.c);
+    if (rc) return rc;
+  }
+  return HPR_OK;
+}
+
+int hpr_group_kkt_origin(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
+  for (auto &rr : g->r) {
+    hpr_ctx *c = rr.c;
+    const hpr_buffers &B = c->B;
+    const int m = (int)c->d.m, n = (int)c->d.n;
+    k_origin_cand<<<grid_for(std::max(m, n)), 256, 0, c->stream>>>(
+        B.cand_y[slot], m, B.cand_z[slot], B.cand_x[slot], term_original ? B.lower : B.lower_s,
+        term_original ? B.upper : B.upper_s, n);
+    CKL();
+    c->launches += 1;
+  }
+  return g_kkt_common(g, term_original, slot, out);
+}
+
+int hpr_group_kkt(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
+  return g_kkt_common(g, term_original, slot, out);
+}
+
+// final unscale (driver.py:382-386) + all-gather of x and z + objectives
+int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out) {
+  int rc = g_check_scaled(g);
+  if (rc) return rc;
+  if (!out || slot < 0 || slot > 1) return fail(HPR_EINVAL, "bad argument");
+  int fs = slot;
+  if (!term_original) {
+    fs = 1 - slot;
+    for (auto &rr : g->r) {
+      hpr_ctx *c = rr.c;
+      const hpr_buffers &B = c->B;
+      const int m = (int)c->d.m, n = (int)c->d.n;
+      k_unscale<<<grid_for(std::max(m, n)), 256, 0, c->stream>>>(
+          B.cand_y[slot], B.cand_z[slot], B.cand_x[slot], B.cand_y[fs], B.cand_z[fs],
+          B.cand_x[fs], B.row_scale, B.col_scale, c->fac, B.lower, B.upper, m, n);
+      CKL();
+      c->launches += 1;
+    }
+  }
+  // x and z are valid on each rank's slice only: gather them
+  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[fs]; },
+                    [&](int l) -> const double * { return g->r[l].c->B.cand_x[fs] + g->j0(l); });
+  if (!rc)
+    rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_z[fs]; },
+                      [&](int l) -> const double * { return g->r[l].c->B.cand_z[fs] + g->j0(l); });
+  if (rc) return rc;
+  return g_kkt_common(g, 1, fs, out);
+}
+
+int hpr_group_last_times(hpr_group *g, double *inner_ms, double *ckpt_ms) {
+  if (!g) return fail(HPR_EINVAL, "null group");
+  return hpr_last_times(g->r[0].c, inner_ms, ckpt_ms);
+}
+
+int hpr_group_launch_count(hpr_group *g, int64_t *count) {
+  if (!g || !count) return fail(HPR_EINVAL, "null argument");
+  int64_t s = 0;
+  for (auto &rr : g->r) s += rr.c->launches;
+  *count = s;
+  return HPR_OK;
+}
+
+}  // extern "C"

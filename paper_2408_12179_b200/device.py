@@ -37,15 +37,34 @@ class DeviceLP:
     """Uploads a reference-shaped LpProblem and owns its native context."""
 
     def __init__(self, problem, device: int = 0, stream=None, pinned_upload: bool = True):
+        ro, ci, v, m, n, m1 = stacked_arrays(problem)
+        rhs = np.concatenate([np.asarray(problem.b_eq, np.float64),
+                              np.asarray(problem.b_ineq, np.float64)])
+        self._setup(ro, ci, v, m, n, m1, rhs, problem.c, problem.lower, problem.upper,
+                    device=device, stream=stream, pinned_upload=pinned_upload)
+
+    @classmethod
+    def from_arrays(cls, ro, ci, v, m, n, m1, b, c, lower, upper, *, device: int = 0,
+                    stream=None, n_alloc: int | None = None, pinned_upload: bool = True):
+        """A row block [rows of A, all n columns] (row-block mode): column vectors
+        are allocated at ``n_alloc >= n`` (the group's padded length)."""
+        self = cls.__new__(cls)
+        self._setup(ro, ci, v, m, n, m1, b, c, lower, upper, device=device, stream=stream,
+                    pinned_upload=pinned_upload, n_alloc=n_alloc)
+        return self
+
+    def _setup(self, ro, ci, v, m, n, m1, rhs, c, lower, upper, *, device, stream,
+               pinned_upload, n_alloc=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise N.NativeUnavailableError("CUDA device required: the HPR-LP path has no CPU fallback")
         N.load_library()
-        ro, ci, v, m, n, m1 = stacked_arrays(problem)
         nnz = int(ro[-1])
         if nnz >= 2**31 - 1 or m >= 2**31 - 1 or n >= 2**31 - 1:
             raise ValueError("problem exceeds int32 indexing of this build")
         self.m, self.n, self.m1, self.nnz = m, n, m1, nnz
+        na = n if n_alloc is None else int(n_alloc)
+        self.n_alloc = na
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
         self.h2d_bytes = 0
@@ -53,15 +72,16 @@ class DeviceLP:
         f64 = dict(dtype=torch.float64, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
         with torch.cuda.stream(self.stream):
-            def up(arr, dtype):
-                t = torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype))
+            def up(arr, dtype, length=None):
+                a = np.ascontiguousarray(arr, dtype=dtype)
+                if length is not None and length > a.size:
+                    a = np.concatenate([a, np.zeros(length - a.size, dtype=dtype)])
+                t = torch.from_numpy(a)
                 if pinned_upload:
                     t = t.pin_memory()
                 self.h2d_bytes += t.numel() * t.element_size()
                 return t.to(dev, non_blocking=True)
 
-            rhs = np.concatenate([np.asarray(problem.b_eq, np.float64),
-                                  np.asarray(problem.b_ineq, np.float64)])
             T = {}
             # nonzero arrays carry PAD trailing slots: the tile engine's bulk copies
             # round every tile up to 16-byte boundaries
@@ -69,9 +89,9 @@ class DeviceLP:
             T["a_ci"] = up(np.concatenate([ci, np.zeros(PAD)]), np.int32)
             T["a_val"] = up(np.concatenate([v, np.zeros(PAD)]), np.float64)
             T["b"] = up(rhs, np.float64)
-            T["c"] = up(problem.c, np.float64)
-            T["lower"] = up(problem.lower, np.float64)
-            T["upper"] = up(problem.upper, np.float64)
+            T["c"] = up(c, np.float64, na)
+            T["lower"] = up(lower, np.float64, na)
+            T["upper"] = up(upper, np.float64, na)
             nz1 = nnz + PAD
             T["a_val_s"] = torch.empty(nz1, **f64)
             T["at_rp"] = torch.empty(n + 1, **i32)
@@ -83,10 +103,10 @@ class DeviceLP:
                 T[name] = torch.empty(m, **f64)
             for name in ("c_s", "lower_s", "upper_s", "col_scale", "x", "anc_x", "w", "xb",
                          "zb", "wtmp"):
-                T[name] = torch.empty(n, **f64)
+                T[name] = torch.empty(na, **f64)
             T["cand_y"] = [torch.empty(m, **f64) for _ in range(2)]
-            T["cand_x"] = [torch.empty(n, **f64) for _ in range(2)]
-            T["cand_z"] = [torch.empty(n, **f64) for _ in range(2)]
+            T["cand_x"] = [torch.empty(na, **f64) for _ in range(2)]
+            T["cand_z"] = [torch.empty(na, **f64) for _ in range(2)]
         self.t = T
         self.dims = N.HprDims(m, n, m1, nnz)
         wsb = ctypes.c_size_t(0)
@@ -186,6 +206,8 @@ class DeviceLP:
         t = self.t[name] if slot is None else self.t[name][slot]
         if name in ("a_ci", "a_val", "a_val_s", "at_ci", "at_perm", "at_val", "at_val_s"):
             t = t[:self.nnz]
+        elif t.numel() == self.n_alloc and self.n_alloc != self.n:
+            t = t[:self.n]
         self.stream.synchronize()
         return t.cpu().numpy()
 
