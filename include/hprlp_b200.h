@@ -261,6 +261,67 @@ int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *
 int hpr_group_last_times(hpr_group *g, double *inner_ms, double *ckpt_ms);
 int hpr_group_launch_count(hpr_group *g, int64_t *count);
 
+/* ------------------------------------------------------------------------
+ * Batch of small LPs (BASELINE config C5; csrc/hpr_batch.cuh): one whole
+ * restarted HPR solve per CTA -- scaling, power method, inner loop,
+ * checkpoints, restarts, sigma updates and the report all on the device.
+ * Replaces `solve` (driver.py:281-405) applied to each LP of the batch.
+ * Every LP must fit one CTA's shared memory (hpr_batch_smem_bytes <= the
+ * device's opt-in maximum, 227 KB on B200: e.g. m=500, n=1000, nnz=5000).
+ * ------------------------------------------------------------------------ */
+typedef struct hpr_batch_problem {
+  int64_t count;
+  int64_t total_rows, total_cols, total_nnz;
+  int32_t max_m, max_n;
+  int64_t max_nnz;
+  const int64_t *row_off, *col_off, *nz_off;   /* count + 1, device */
+  const int32_t *m1;                           /* count: equality rows of each LP */
+  const int32_t *rp;      /* total_rows + count: LP i's m_i + 1 local row pointers at row_off[i] + i */
+  const int32_t *ci;      /* total_nnz: local column ids, strictly increasing within a row */
+  const double *val;      /* total_nnz */
+  const double *b;        /* total_rows */
+  const double *c, *lower, *upper;             /* total_cols */
+  const double *obj_const;                     /* count */
+  const int32_t *obj_neg;                      /* count: 1 = MAX problem (report negated) */
+} hpr_batch_problem;
+
+#define HPR_BATCH_DR 0
+#define HPR_BATCH_HDR_FIXED 1
+#define HPR_BATCH_HDR 2
+#define HPR_BATCH_HPR 3
+
+typedef struct hpr_batch_config {   /* SolverConfig (driver.py:50-68) */
+  double tolerance, time_limit_seconds, alpha1, alpha2, alpha3, sigma0, power_tol;
+  int64_t max_iterations;
+  int32_t check_interval, variant, ruiz_iters, pock_chambolle, bc_normalize, power_max_iters;
+  int32_t term_original;   /* termination_space == "original" */
+  int32_t max_log;         /* restart records kept per LP */
+} hpr_batch_config;
+
+typedef struct hpr_restart_rec {    /* RestartEvent (driver.py:117-127) */
+  int32_t outer_index, trigger;     /* 0 sufficient, 1 stalled, 2 long_loop */
+  int64_t tau;
+  double sigma_next, merit;
+} hpr_restart_rec;
+
+typedef struct hpr_batch_result {   /* SolveReport fields (driver.py:154-188) */
+  int32_t status;                   /* 0 Optimal, 1 IterationLimit, 2 TimeLimit, 3 NumericalError */
+  int32_t restarts;
+  int64_t iterations;
+  int32_t power_iterations, power_converged, dual_clamped, n_log, merit_negative, power_failed;
+  double primal_objective, dual_objective;
+  double kkt[9];   /* primal abs/rel, dual abs/rel, gap abs/rel, residual norm, pobj, dobj */
+  double sigma_final, lambda_estimate, lambda_raw, b_factor, c_factor, device_seconds;
+} hpr_batch_result;
+
+int hpr_batch_smem_bytes(int32_t max_m, int32_t max_n, int64_t max_nnz, size_t *bytes);
+int hpr_batch_workspace_bytes(const hpr_batch_problem *p, size_t *bytes);
+/* Asynchronous on `stream`.  results[count]; log[count * max_log]; x, z
+ * (total_cols) and y (total_rows) receive each LP's solution. */
+int hpr_batch_solve(const hpr_batch_problem *p, const hpr_batch_config *cfg, void *workspace,
+                    size_t ws_bytes, hpr_batch_result *results, hpr_restart_rec *log,
+                    double *x, double *y, double *z, int device, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,43 @@ class HprLayoutInfo(ctypes.Structure):
                                                "long_rows_a", "long_rows_at")]
 
 
+class HprBatchProblem(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("total_rows", ctypes.c_int64),
+                ("total_cols", ctypes.c_int64), ("total_nnz", ctypes.c_int64),
+                ("max_m", ctypes.c_int32), ("max_n", ctypes.c_int32), ("max_nnz", ctypes.c_int64),
+                ("row_off", ctypes.c_void_p), ("col_off", ctypes.c_void_p),
+                ("nz_off", ctypes.c_void_p), ("m1", ctypes.c_void_p), ("rp", ctypes.c_void_p),
+                ("ci", ctypes.c_void_p), ("val", ctypes.c_void_p), ("b", ctypes.c_void_p),
+                ("c", ctypes.c_void_p), ("lower", ctypes.c_void_p), ("upper", ctypes.c_void_p),
+                ("obj_const", ctypes.c_void_p), ("obj_neg", ctypes.c_void_p)]
+
+
+class HprBatchConfig(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_double) for f in ("tolerance", "time_limit_seconds", "alpha1",
+                                                "alpha2", "alpha3", "sigma0", "power_tol")] + [
+        ("max_iterations", ctypes.c_int64)] + [
+        (f, ctypes.c_int32) for f in ("check_interval", "variant", "ruiz_iters", "pock_chambolle",
+                                      "bc_normalize", "power_max_iters", "term_original",
+                                      "max_log")]
+
+
+class HprRestartRec(ctypes.Structure):
+    _fields_ = [("outer_index", ctypes.c_int32), ("trigger", ctypes.c_int32),
+                ("tau", ctypes.c_int64), ("sigma_next", ctypes.c_double),
+                ("merit", ctypes.c_double)]
+
+
+class HprBatchResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("restarts", ctypes.c_int32),
+                ("iterations", ctypes.c_int64)] + [
+        (f, ctypes.c_int32) for f in ("power_iterations", "power_converged", "dual_clamped",
+                                      "n_log", "merit_negative", "power_failed")] + [
+        ("primal_objective", ctypes.c_double), ("dual_objective", ctypes.c_double),
+        ("kkt", ctypes.c_double * 9)] + [
+        (f, ctypes.c_double) for f in ("sigma_final", "lambda_estimate", "lambda_raw",
+                                       "b_factor", "c_factor", "device_seconds")]
+
+
 # name -> (restype, argtypes); every int-returning function is error-checked
 _SIGS = {
     "hpr_abi_version": (ctypes.c_int, []),
@@ -144,6 +181,16 @@ _SIGS = {
     "hpr_group_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double)]),
     "hpr_group_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    # batch of small LPs (hpr_batch.cuh)
+    "hpr_batch_smem_bytes": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                            ctypes.POINTER(ctypes.c_size_t)]),
+    "hpr_batch_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(HprBatchProblem),
+                                                 ctypes.POINTER(ctypes.c_size_t)]),
+    "hpr_batch_solve": (ctypes.c_int, [ctypes.POINTER(HprBatchProblem),
+                                       ctypes.POINTER(HprBatchConfig), ctypes.c_void_p,
+                                       ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_int, ctypes.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

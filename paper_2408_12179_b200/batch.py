@@ -1,0 +1,225 @@
+"""Batch of small LPs, one whole restarted HPR solve per CTA (config C5).
+
+``solve_batch(problems, cfg)`` is ``[solve(p, cfg) for p in problems]``
+(reference ``driver.py:281-405`` per LP) executed as ONE kernel launch of
+``libhprlp_b200.so`` (``csrc/hpr_batch.cuh``): each CTA stages its LP in
+shared memory and runs scaling, the power method, the inner loop, the
+checkpoints, restarts and sigma updates without returning to the host.
+``solve_batch_sharded`` splits the batch across the ranks of a
+``torch.distributed`` job (independent units, no data-path collective).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import warnings
+
+import numpy as np
+
+from . import _native as N
+from .driver import (KktResidual, RestartEvent, SolveReport, SolverConfig, SolveStatus, Timings,
+                     Variant)
+from .problem import PrimalDualPoint, stacked_arrays
+
+_STATUS = {0: SolveStatus.OPTIMAL, 1: SolveStatus.ITERATION_LIMIT, 2: SolveStatus.TIME_LIMIT,
+           3: SolveStatus.NUMERICAL_ERROR}
+_TRIGGER = {0: "sufficient", 1: "stalled", 2: "long_loop"}
+_VARIANT = {Variant.DR: 0, Variant.HDR_FIXED_SIGMA: 1, Variant.HDR: 2, Variant.HPR: 3}
+MAX_LOG = 64
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class PackedBatch:
+    """Host-side concatenation of a list of reference-shaped LPs."""
+
+    def __init__(self, problems):
+        if not problems:
+            raise ValueError("empty batch")
+        rps, cis, vals, bs, cs, ls, us = [], [], [], [], [], [], []
+        ms, ns, nzs, m1s, oc, neg = [], [], [], [], [], []
+        for p in problems:
+            ro, ci, v, m, n, m1 = stacked_arrays(p)
+            if int(ro[-1]) == 0:
+                raise ValueError("matrix must be non-zero")
+            rps.append(np.asarray(ro, np.int32))
+            cis.append(np.asarray(ci, np.int32))
+            vals.append(np.asarray(v, np.float64))
+            bs.append(np.concatenate([np.asarray(p.b_eq, np.float64),
+                                      np.asarray(p.b_ineq, np.float64)]))
+            cs.append(np.asarray(p.c, np.float64))
+            ls.append(np.asarray(p.lower, np.float64))
+            us.append(np.asarray(p.upper, np.float64))
+            ms.append(m)
+            ns.append(n)
+            nzs.append(int(ro[-1]))
+            m1s.append(m1)
+            oc.append(float(getattr(p, "objective_constant", 0.0)))
+            neg.append(int(bool(getattr(p, "objective_negated", False))))
+        self.count = len(problems)
+        self.m = np.asarray(ms, np.int64)
+        self.n = np.asarray(ns, np.int64)
+        self.nnz = np.asarray(nzs, np.int64)
+        self.row_off = np.concatenate([[0], np.cumsum(self.m)]).astype(np.int64)
+        self.col_off = np.concatenate([[0], np.cumsum(self.n)]).astype(np.int64)
+        self.nz_off = np.concatenate([[0], np.cumsum(self.nnz)]).astype(np.int64)
+        self.arrays = {
+            "row_off": self.row_off, "col_off": self.col_off, "nz_off": self.nz_off,
+            "m1": np.asarray(m1s, np.int32), "rp": np.concatenate(rps),
+            "ci": np.concatenate(cis), "val": np.concatenate(vals), "b": np.concatenate(bs),
+            "c": np.concatenate(cs), "lower": np.concatenate(ls), "upper": np.concatenate(us),
+            "obj_const": np.asarray(oc, np.float64), "obj_neg": np.asarray(neg, np.int32)}
+
+    def h2d_bytes(self):
+        return sum(a.nbytes for a in self.arrays.values())
+
+
+def _config(cfg: SolverConfig, max_log: int) -> N.HprBatchConfig:
+    c = N.HprBatchConfig()
+    c.tolerance = cfg.tolerance
+    c.time_limit_seconds = cfg.time_limit_seconds
+    c.alpha1, c.alpha2, c.alpha3 = cfg.alpha1, cfg.alpha2, cfg.alpha3
+    c.sigma0 = cfg.sigma0
+    c.power_tol = cfg.power_tol
+    c.max_iterations = int(cfg.max_iterations)
+    c.check_interval = int(cfg.check_interval)
+    c.variant = _VARIANT[cfg.variant]
+    c.ruiz_iters = int(cfg.ruiz_iters)
+    c.pock_chambolle = int(bool(cfg.pock_chambolle))
+    c.bc_normalize = int(bool(cfg.bc_normalize))
+    c.power_max_iters = int(cfg.power_max_iters)
+    c.term_original = int(cfg.termination_space == "original")
+    c.max_log = int(max_log)
+    return c
+
+
+class BatchRun:
+    """Device residency of one packed batch + its native solve (re-runnable)."""
+
+    def __init__(self, packed: PackedBatch, device: int = 0, stream=None, pinned: bool = True):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise N.NativeUnavailableError("CUDA device required: the batch path has no CPU fallback")
+        N.load_library()
+        self.packed = packed
+        self.device = torch.device("cuda", device)
+        self.dev_index = device
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.t = {}
+        with torch.cuda.stream(self.stream):
+            for k, a in packed.arrays.items():
+                h = torch.from_numpy(np.ascontiguousarray(a))
+                if pinned:
+                    h = h.pin_memory()
+                self.t[k] = h.to(self.device, non_blocking=True)
+        self.h2d_bytes = packed.h2d_bytes()
+        pb = N.HprBatchProblem()
+        pb.count = packed.count
+        pb.total_rows = int(packed.row_off[-1])
+        pb.total_cols = int(packed.col_off[-1])
+        pb.total_nnz = int(packed.nz_off[-1])
+        pb.max_m = int(packed.m.max())
+        pb.max_n = int(packed.n.max())
+        pb.max_nnz = int(packed.nnz.max())
+        for k in ("row_off", "col_off", "nz_off", "m1", "rp", "ci", "val", "b", "c", "lower",
+                  "upper", "obj_const", "obj_neg"):
+            setattr(pb, k, self.t[k].data_ptr())
+        self.pb = pb
+        wsb = ctypes.c_size_t(0)
+        N.call("hpr_batch_workspace_bytes", ctypes.byref(pb), ctypes.byref(wsb))
+        f64 = dict(dtype=torch.float64, device=self.device)
+        with torch.cuda.stream(self.stream):
+            self.ws = torch.empty(int(wsb.value), dtype=torch.uint8, device=self.device)
+            self.x = torch.empty(max(pb.total_cols, 1), **f64)
+            self.z = torch.empty(max(pb.total_cols, 1), **f64)
+            self.y = torch.empty(max(pb.total_rows, 1), **f64)
+            self.res = torch.empty(packed.count * ctypes.sizeof(N.HprBatchResult),
+                                   dtype=torch.uint8, device=self.device)
+            self.log = torch.empty(packed.count * MAX_LOG * ctypes.sizeof(N.HprRestartRec),
+                                   dtype=torch.uint8, device=self.device)
+        self.launches = 0
+
+    def launch(self, cfg: SolverConfig):
+        c = _config(cfg, MAX_LOG)
+        N.call("hpr_batch_solve", ctypes.byref(self.pb), ctypes.byref(c),
+               ctypes.c_void_p(self.ws.data_ptr()), ctypes.c_size_t(self.ws.numel()),
+               ctypes.c_void_p(self.res.data_ptr()), ctypes.c_void_p(self.log.data_ptr()),
+               ctypes.c_void_p(self.x.data_ptr()), ctypes.c_void_p(self.y.data_ptr()),
+               ctypes.c_void_p(self.z.data_ptr()), self.dev_index,
+               ctypes.c_void_p(self.stream.cuda_stream))
+        # transpose keys + iota + cub sort (3) + col count + gather + rpt + solve
+        self.launches += 9
+
+    def reports(self, cfg: SolverConfig) -> list[SolveReport]:
+        self.stream.synchronize()
+        pk = self.packed
+        raw = self.res.cpu().numpy().tobytes()
+        lraw = self.log.cpu().numpy().tobytes()
+        x, y, z = self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy()
+        rs = (N.HprBatchResult * pk.count).from_buffer_copy(raw)
+        recs = (N.HprRestartRec * (pk.count * MAX_LOG)).from_buffer_copy(lraw)
+        out = []
+        for i in range(pk.count):
+            r = rs[i]
+            if r.power_iterations and not r.power_converged:
+                warnings.warn(f"power method did not converge within {r.power_iterations} "
+                              "iterations", RuntimeWarning)
+            if r.merit_negative:
+                warnings.warn("negative quadratic form in the merit: lambda may underestimate "
+                              "lambda_1(AA*)", RuntimeWarning)
+            k = list(r.kkt)
+            kkt = KktResidual(k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8],
+                              int(r.dual_clamped))
+            log = []
+            for q in range(min(r.n_log, MAX_LOG)):
+                e = recs[i * MAX_LOG + q]
+                log.append(RestartEvent(int(e.outer_index), _TRIGGER[int(e.trigger)], int(e.tau),
+                                        float(e.sigma_next), float(e.merit)))
+            c0, c1 = int(pk.col_off[i]), int(pk.col_off[i + 1])
+            r0, r1 = int(pk.row_off[i]), int(pk.row_off[i + 1])
+            sol = PrimalDualPoint(y=y[r0:r1].copy(), z=z[c0:c1].copy(), x=x[c0:c1].copy())
+            tm = Timings(iteration_seconds=float(r.device_seconds))
+            out.append(SolveReport(
+                status=_STATUS[int(r.status)], primal_objective=float(r.primal_objective),
+                dual_objective=float(r.dual_objective), kkt=kkt, iterations=int(r.iterations),
+                restarts=int(r.restarts), restart_log=log, timings=tm, solution=sol,
+                sigma_final=float(r.sigma_final), lambda_estimate=float(r.lambda_estimate),
+                device_stats={"lambda_raw": float(r.lambda_raw),
+                              "power_iterations": int(r.power_iterations),
+                              "b_factor": float(r.b_factor), "c_factor": float(r.c_factor),
+                              "batch_index": i}))
+        return out
+
+
+def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
+    """``[solve(p, cfg) for p in problems]`` as one device launch (one CTA per LP)."""
+    cfg = SolverConfig.coerce(cfg)
+    if math.isfinite(cfg.time_limit_seconds):
+        warnings.warn("batch time limits are measured per CTA on the device clock",
+                      RuntimeWarning)
+    run = BatchRun(PackedBatch(list(problems)), device=device)
+    run.launch(cfg)
+    return run.reports(cfg)
+
+
+def shard_bounds(count: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced shard [lo, hi) of ``count`` LPs for ``rank``."""
+    base, extra = divmod(count, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def solve_batch_sharded(problems, cfg=None, *, device: int | None = None):
+    """Each rank of a torch.distributed job solves its shard; returns this
+    rank's reports and its [lo, hi) range (no data-path collective)."""
+    import os
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    lo, hi = shard_bounds(len(problems), world, rank)
+    return solve_batch(problems[lo:hi], cfg, device=device), (lo, hi)

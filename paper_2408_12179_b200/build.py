@@ -11,6 +11,7 @@ ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
               os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
+              os.path.join(HERE, "csrc", "hpr_batch.cuh"),
               os.path.join(ROOT, "include", "hprlp_b200.h")]
 OUT = os.path.join(HERE, "libhprlp_b200.so")
 

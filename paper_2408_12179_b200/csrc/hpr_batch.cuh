@@ -1,0 +1,780 @@
+// hpr_batch.cuh -- K11: a batch of small LPs, one whole restarted HPR solve per CTA
+// (BASELINE config C5: 4096 x (m=500, n=1000, nnz=5000)).
+//
+// Included at the end of hpr_capi.cu.  Each CTA owns one LP for the whole
+// solve: it stages the LP's CSR A and CSR A^T (scaled values), the iterate, the
+// anchors and the scaled problem vectors in shared memory (~210 KB at C5) and
+// runs the reference's complete pipeline on the SM with no host round trip:
+//
+//   scale_problem            scaling.py:72-125 (Ruiz x10, Pock-Chambolle, b/c norm)
+//   power_method_lambda_max  sparse.py:165-203
+//   the restarted loop       driver.py:317-372 (iterate_once core.py:163-174,
+//                            half_step 118-129, kkt_residual driver.py:191-228,
+//                            merit core.py:182-218, restart rules 238-248,
+//                            sigma update 251-278, status priority 341-346)
+//   the report               driver.py:374-391
+//
+// Arithmetic order is the single-LP path's: every sparse product is a
+// sequential left-to-right sum of separately rounded products (scipy
+// csr_matvec), one thread per row (x-phase: per column over A^T).  Norms and
+// dots are fixed-order block reductions (warp shuffle tree, then the 16 warp
+// partials summed in warp order), evaluated identically by every thread so the
+// scalar decisions need no broadcast.  Original-value KKT terms read A and A^T
+// from global memory (L2) at checkpoints only.
+#pragma once
+
+namespace hpr {
+namespace batch {
+
+constexpr int kBT = 512;            // threads per CTA (one LP)
+constexpr int kBW = kBT / 32;
+
+struct Prob {
+  const int64_t *row_off, *col_off, *nz_off;
+  const int *m1;
+  const int *rp;                    // LP i's local row pointers at row_off[i] + i
+  const int *ci;
+  const double *val;
+  const int *grpt;                  // transpose row pointers (global positions), col_off[i] + i
+  const int *cit;                   // transpose column indices (local rows)
+  const double *valt;               // transpose original values
+  const double *b, *c, *lo, *up;
+  const double *obj_const;
+  const int *obj_neg;
+};
+
+struct Cfg {
+  double tol, time_limit, a1, a2, a3, sigma0, power_tol;
+  long long max_iter;
+  int check_interval, variant, uses_restarts, updates_sigma;
+  int ruiz, pc, bc, power_max, term_original, max_log;
+};
+
+struct Out {
+  hpr_batch_result *res;
+  hpr_restart_rec *log;
+  double *x, *y, *z;                // solution (also the checkpoint candidate)
+  double *dy;                       // scratch, row-indexed
+};
+
+// fixed-order block sum of NQ values; every thread receives the totals
+template <int NQ>
+__device__ __forceinline__ void bsum(double (&v)[NQ], double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double a = v[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, off));
+    if (lane == 0) red[q * kBW + warp] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double s = 0.0;
+    for (int w = 0; w < kBW; ++w) s = __dadd_rn(s, red[q * kBW + w]);
+    v[q] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// sequential sum of row r of a shared-memory CSR against vector v
+__device__ __forceinline__ double srow(const int *rp, const int *ci, const double *val,
+                                       const double *v, int r) {
+  double s = 0.0;
+  const int e1 = rp[r + 1];
+  for (int e = rp[r]; e < e1; ++e) s = __dadd_rn(s, __dmul_rn(val[e], v[ci[e]]));
+  return s;
+}
+
+// same for a global-memory CSR (original values at checkpoints); v in global
+// memory written earlier by this CTA (plain coherent loads, no __ldg)
+__device__ __forceinline__ double grow(const int *rp, int base, const int *ci, const double *val,
+                                       const double *v, int r) {
+  double s = 0.0;
+  const int e1 = rp[r + 1] - base;
+  for (int e = rp[r] - base; e < e1; ++e) s = __dadd_rn(s, __dmul_rn(val[e], v[ci[e]]));
+  return s;
+}
+
+size_t smem_bytes(int m, int n, long long nnz) {
+  size_t b = 0;
+  b += 2 * (size_t)nnz * 8;                    // av, atv
+  b += 8 * (size_t)(5 * m + 8 * n);            // y ay bs yb rs | x ax w cs ls us csc xb
+  b += 2 * (size_t)nnz * 4;                    // aci, atci
+  b += 4 * (size_t)(m + 1 + n + 1);            // arp, atrp
+  b = (b + 15) / 16 * 16;
+  b += 8 * (size_t)24 * kBW;                   // reduction scratch
+  return b;
+}
+
+__global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int lp = blockIdx.x, tid = threadIdx.x;
+  const unsigned long long t_start = gtimer();
+  const long long r0 = P.row_off[lp], c0 = P.col_off[lp], z0 = P.nz_off[lp];
+  const int m = (int)(P.row_off[lp + 1] - r0), n = (int)(P.col_off[lp + 1] - c0);
+  const int nnz = (int)(P.nz_off[lp + 1] - z0);
+  const int m1 = P.m1[lp];
+  // ---- carve shared memory ----
+  double *p = (double *)smraw;
+  double *av = p; p += nnz;
+  double *atv = p; p += nnz;
+  double *y = p; p += m;
+  double *ay = p; p += m;
+  double *bs = p; p += m;
+  double *yb = p; p += m;
+  double *rs = p; p += m;
+  double *x = p; p += n;
+  double *ax = p; p += n;
+  double *w = p; p += n;
+  double *cs = p; p += n;
+  double *ls = p; p += n;
+  double *us = p; p += n;
+  double *csc = p; p += n;
+  double *xb = p; p += n;
+  int *ip = (int *)p;
+  int *aci = ip; ip += nnz;
+  int *atci = ip; ip += nnz;
+  int *arp = ip; ip += m + 1;
+  int *atrp = ip; ip += n + 1;
+  double *red = (double *)(((uintptr_t)ip + 15) & ~(uintptr_t)15);
+  // global views of this LP
+  const int *grp = P.rp + r0 + lp;             // local row pointers (m + 1)
+  const int *gci = P.ci + z0;
+  const double *gval = P.val + z0;
+  const int *gtrp = P.grpt + c0 + lp;          // global positions (n + 1)
+  const int *gtci = P.cit + z0;
+  const double *gtval = P.valt + z0;
+  const double *b0 = P.b + r0, *c0v = P.c + c0, *l0 = P.lo + c0, *u0 = P.up + c0;
+  double *ox = O.x + c0, *oy = O.y + r0, *oz = O.z + c0, *gdy = O.dy + r0;
+  const int tz = (int)z0;
+
+  for (int e = tid; e < nnz; e += kBT) {
+    aci[e] = gci[e];
+    av[e] = gval[e];
+    atci[e] = gtci[e];
+    atv[e] = gtval[e];
+  }
+  for (int i = tid; i <= m; i += kBT) arp[i] = grp[i];
+  for (int j = tid; j <= n; j += kBT) atrp[j] = gtrp[j] - tz;
+  for (int i = tid; i < m; i += kBT) rs[i] = 1.0;
+  for (int j = tid; j < n; j += kBT) csc[j] = 1.0;
+  __syncthreads();
+
+  // ---- scale_problem (scaling.py:81-103) ----
+  // one pass: row divisors in yb, column divisors in xb, then both value copies
+  // become (v / dr[row]) / dc[col]
+  auto apply_pass = [&]() {
+    for (int i = tid; i < m; i += kBT) {
+      const double d = yb[i];
+      rs[i] = __dmul_rn(rs[i], d);
+      for (int e = arp[i]; e < arp[i + 1]; ++e) av[e] = __ddiv_rn(__ddiv_rn(av[e], d), xb[aci[e]]);
+    }
+    for (int j = tid; j < n; j += kBT) {
+      const double d = xb[j];
+      csc[j] = __dmul_rn(csc[j], d);
+      for (int e = atrp[j]; e < atrp[j + 1]; ++e)
+        atv[e] = __ddiv_rn(__ddiv_rn(atv[e], yb[atci[e]]), d);
+    }
+    __syncthreads();
+  };
+  for (int it = 0; it < C.ruiz; ++it) {
+    for (int i = tid; i < m; i += kBT) {
+      double mx = 0.0;
+      for (int e = arp[i]; e < arp[i + 1]; ++e) mx = fmax(mx, fabs(av[e]));
+      double d = sqrt(mx);
+      yb[i] = d == 0.0 ? 1.0 : d;
+    }
+    for (int j = tid; j < n; j += kBT) {
+      double mx = 0.0;
+      for (int e = atrp[j]; e < atrp[j + 1]; ++e) mx = fmax(mx, fabs(atv[e]));
+      double d = sqrt(mx);
+      xb[j] = d == 0.0 ? 1.0 : d;
+    }
+    __syncthreads();
+    apply_pass();
+  }
+  if (C.pc) {
+    for (int i = tid; i < m; i += kBT) {
+      double s = 0.0;
+      for (int e = arp[i]; e < arp[i + 1]; ++e) s = __dadd_rn(s, fabs(av[e]));
+      double d = sqrt(s);
+      yb[i] = d == 0.0 ? 1.0 : d;
+    }
+    for (int j = tid; j < n; j += kBT) {
+      double s = 0.0;
+      for (int e = atrp[j]; e < atrp[j + 1]; ++e) s = __dadd_rn(s, fabs(atv[e]));
+      double d = sqrt(s);
+      xb[j] = d == 0.0 ? 1.0 : d;
+    }
+    __syncthreads();
+    apply_pass();
+  }
+  for (int i = tid; i < m; i += kBT) bs[i] = __ddiv_rn(b0[i], rs[i]);
+  for (int j = tid; j < n; j += kBT) {
+    cs[j] = __ddiv_rn(c0v[j], csc[j]);
+    ls[j] = __dmul_rn(l0[j], csc[j]);
+    us[j] = __dmul_rn(u0[j], csc[j]);
+  }
+  __syncthreads();
+  double bf = 1.0, cf = 1.0;
+  if (C.bc) {
+    double v2[2] = {0.0, 0.0};
+    for (int i = tid; i < m; i += kBT) v2[0] = __dadd_rn(v2[0], sq(bs[i]));
+    for (int j = tid; j < n; j += kBT) v2[1] = __dadd_rn(v2[1], sq(cs[j]));
+    bsum<2>(v2, red);
+    bf = __dadd_rn(sqrt(v2[0]), 1.0);
+    cf = __dadd_rn(sqrt(v2[1]), 1.0);
+    for (int i = tid; i < m; i += kBT) bs[i] = __ddiv_rn(bs[i], bf);
+    for (int j = tid; j < n; j += kBT) {
+      cs[j] = __ddiv_rn(cs[j], cf);
+      ls[j] = __ddiv_rn(ls[j], bf);
+      us[j] = __ddiv_rn(us[j], bf);
+    }
+    __syncthreads();
+  }
+  // ||b||, ||c|| of the termination problem (relative residual denominators)
+  double bnorm, cnorm;
+  {
+    double v2[2] = {0.0, 0.0};
+    for (int i = tid; i < m; i += kBT) v2[0] = __dadd_rn(v2[0], sq(C.term_original ? b0[i] : bs[i]));
+    for (int j = tid; j < n; j += kBT) v2[1] = __dadd_rn(v2[1], sq(C.term_original ? c0v[j] : cs[j]));
+    bsum<2>(v2, red);
+    bnorm = sqrt(v2[0]);
+    cnorm = sqrt(v2[1]);
+  }
+
+  // ---- power method (sparse.py:165-203): v in yb, u in w, A u in ay ----
+  int start = -2;
+  for (int fb = -1; fb < m; ++fb) {
+    for (int i = tid; i < m; i += kBT) yb[i] = fb < 0 ? 1.0 : (i == fb ? 1.0 : 0.0);
+    __syncthreads();
+    double u2[1] = {0.0};
+    for (int j = tid; j < n; j += kBT) u2[0] = __dadd_rn(u2[0], sq(srow(atrp, atci, atv, yb, j)));
+    bsum<1>(u2, red);
+    if (sqrt(u2[0]) > 0.0) {
+      start = fb;
+      break;
+    }
+  }
+  double lam = 0.0, lam_prev = 0.0;
+  int piters = 0, pconv = 0;
+  if (start == -1) {
+    const double inv = 1.0 / sqrt((double)m);
+    for (int i = tid; i < m; i += kBT) yb[i] = inv;
+  }
+  __syncthreads();
+  if (start != -2) {
+    for (int it = 1; it <= C.power_max; ++it) {
+      piters = it;
+      for (int j = tid; j < n; j += kBT) w[j] = srow(atrp, atci, atv, yb, j);
+      __syncthreads();
+      double d2[2] = {0.0, 0.0};
+      for (int i = tid; i < m; i += kBT) {
+        const double s = srow(arp, aci, av, w, i);
+        ay[i] = s;
+        d2[0] = __dadd_rn(d2[0], __dmul_rn(yb[i], s));
+        d2[1] = __dadd_rn(d2[1], sq(s));
+      }
+      bsum<2>(d2, red);
+      lam = d2[0];
+      const double nw = sqrt(d2[1]);
+      if (nw == 0.0) break;
+      for (int i = tid; i < m; i += kBT) yb[i] = __ddiv_rn(ay[i], nw);
+      __syncthreads();
+      if (it > 1 && fabs(__dsub_rn(lam, lam_prev)) <= __dmul_rn(C.power_tol, fmax(fabs(lam), 1e-300))) {
+        pconv = 1;
+        break;
+      }
+      lam_prev = lam;
+    }
+  }
+  const double lam_raw = lam;
+  const double lamv = lam * (1.0 + 1e-3);
+
+  // ---- state (SolverState.origin, core.py:110-115) ----
+  for (int i = tid; i < m; i += kBT) y[i] = ay[i] = 0.0;
+  for (int j = tid; j < n; j += kBT) x[j] = ax[j] = 0.0;
+  __syncthreads();
+  double sigma = C.sigma0;
+  long long k = 0, t = 0;
+  int r = 0, status = -1, nlog = 0, have_ckpt = 0, merit_neg = 0;
+  bool have_first = false;
+  double merit_first = 0.0, merit_prev = INFINITY;
+  double kk[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double lz = 0.0, uz = 0.0;
+  long long clamped = 0;
+  const double oc = P.obj_const[lp];
+  const bool term_orig = C.term_original != 0;
+
+  // KKT terms of the candidate in (oy, oz, ox) on the termination problem;
+  // results into kk[] (driver.py:203-216)
+  auto kkt = [&](double (&s)[11]) {
+    for (int i = tid; i < m; i += kBT) {
+      const double axi = term_orig ? grow(grp, 0, gci, gval, ox, i) : srow(arp, aci, av, ox, i);
+      const double bi = term_orig ? b0[i] : bs[i];
+      const double yi = oy[i];
+      double prim = __dsub_rn(bi, axi);
+      double tproj = __dadd_rn(__dsub_rn(yi, axi), bi);
+      if (i >= m1) {
+        prim = np_max(prim, 0.0);
+        tproj = np_max(tproj, 0.0);
+      }
+      s[0] = __dadd_rn(s[0], sq(prim));
+      s[1] = __dadd_rn(s[1], __dmul_rn(bi, yi));
+      s[2] = __dadd_rn(s[2], sq(__dsub_rn(yi, tproj)));
+    }
+    for (int j = tid; j < n; j += kBT) {
+      const double aty = term_orig ? grow(gtrp, tz, gtci, gtval, oy, j) : srow(atrp, atci, atv, oy, j);
+      const double cj = term_orig ? c0v[j] : cs[j];
+      const double l = term_orig ? l0[j] : ls[j];
+      const double u = term_orig ? u0[j] : us[j];
+      const double zj = oz[j], xj = ox[j];
+      s[3] = __dadd_rn(s[3], sq(__dsub_rn(__dsub_rn(cj, aty), zj)));
+      s[4] = __dadd_rn(s[4], __dmul_rn(cj, xj));
+      if (zj > 0.0) {
+        if (isfinite(l)) {
+          s[5] = __dadd_rn(s[5], __dmul_rn(l, zj));
+          s[7] += 1.0;
+        } else {
+          s[9] += 1.0;
+        }
+      } else if (zj < 0.0) {
+        if (isfinite(u)) {
+          s[6] = __dadd_rn(s[6], __dmul_rn(u, zj));
+          s[8] += 1.0;
+        } else {
+          s[9] += 1.0;
+        }
+      }
+      s[10] = __dadd_rn(s[10], sq(__dsub_rn(xj, np_clip(__dsub_rn(xj, zj), l, u))));
+    }
+  };
+  auto kkt_finish = [&](const double (&s)[11]) {
+    // s: prim2 by r1 dual2 cx lz uz nlo nup clamped r2   (kkt_from_sums)
+    const double pa = sqrt(s[0]);
+    const double pr = pa / (1.0 + bnorm);
+    const double da = sqrt(s[3]);
+    const double dr = da / (1.0 + cnorm);
+    const double pobj = s[4] + oc;
+    double dobj = s[1];
+    if (s[7] != 0.0) dobj += s[5];
+    if (s[8] != 0.0) dobj += s[6];
+    dobj += oc;
+    const double ga = fabs(dobj - pobj);
+    const double gr = ga / (1.0 + fabs(dobj) + fabs(pobj));
+    kk[0] = pa; kk[1] = pr; kk[2] = da; kk[3] = dr; kk[4] = ga; kk[5] = gr;
+    kk[6] = sqrt(s[2] + s[10] + s[3]);
+    kk[7] = pobj; kk[8] = dobj;
+    lz = s[5]; uz = s[6];
+    clamped = (long long)s[9];
+  };
+
+  while (status < 0) {
+    const long long steps = C.max_iter - k < C.check_interval ? C.max_iter - k : C.check_interval;
+    const double lamsig = lamv * sigma;
+    bool broke = false;
+    for (long long st = 0; st < steps; ++st) {
+      const double t2 = (double)t + 2.0;
+      const double wn = ((double)t + 1.0) / t2, wa = 1.0 / t2;
+      int bad = 0;
+      for (int j = tid; j < n; j += kBT) {       // x phase (core.py:168-169)
+        const double aty = srow(atrp, atci, atv, y, j);
+        const double xj = x[j];
+        const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
+        const double xbj = np_clip(v, ls[j], us[j]);
+        const double wj = __dsub_rn(__dmul_rn(2.0, xbj), xj);
+        const double xn = C.variant == 0 ? xbj
+                                         : __dadd_rn(__dmul_rn(wa, ax[j]), __dmul_rn(wn, C.variant == 2 ? wj : xbj));
+        w[j] = wj;
+        x[j] = xn;
+        bad |= !isfinite(xn);
+      }
+      __syncthreads();
+      for (int i = tid; i < m; i += kBT) {       // y phase (core.py:170-172)
+        const double s = srow(arp, aci, av, w, i);
+        const double yi = y[i];
+        double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
+        if (i >= m1) ybi = np_max(ybi, 0.0);
+        double yn = ybi;
+        if (C.variant != 0) {
+          const double tg = C.variant == 2 ? __dsub_rn(__dmul_rn(2.0, ybi), yi) : ybi;
+          yn = __dadd_rn(__dmul_rn(wa, ay[i]), __dmul_rn(wn, tg));
+        }
+        y[i] = yn;
+        bad |= !isfinite(yn);
+      }
+      if (__syncthreads_or(bad)) {              // NumericalBreakdownError(k)
+        broke = true;
+        break;
+      }
+      ++t;
+      ++k;
+    }
+    if (broke) {
+      status = 3;
+      break;
+    }
+    // ---- checkpoint: half step (core.py:118-129) + candidate (driver.py:333-336) ----
+    double s17[17];
+#pragma unroll
+    for (int q = 0; q < 17; ++q) s17[q] = 0.0;
+    for (int j = tid; j < n; j += kBT) {
+      const double aty = srow(atrp, atci, atv, y, j);
+      const double xj = x[j];
+      const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
+      const double xbj = np_clip(v, ls[j], us[j]);
+      const double zbj = __ddiv_rn(__dsub_rn(xbj, v), sigma);
+      xb[j] = xbj;
+      w[j] = __dsub_rn(__dmul_rn(2.0, xbj), xj);
+      s17[0] = __dadd_rn(s17[0], sq(__dsub_rn(xbj, ax[j])));     // bar_dx2
+      s17[1] = __dadd_rn(s17[1], sq(__dsub_rn(xj, xbj)));        // dx2
+      if (term_orig) {
+        const double cj = csc[j];
+        ox[j] = np_clip(__dmul_rn(xbj, __ddiv_rn(bf, cj)), l0[j], u0[j]);
+        oz[j] = __dmul_rn(zbj, __dmul_rn(cf, cj));
+      } else {
+        ox[j] = xbj;
+        oz[j] = zbj;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += kBT) {
+      const double s = srow(arp, aci, av, w, i);
+      const double yi = y[i];
+      double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
+      if (i >= m1) ybi = np_max(ybi, 0.0);
+      const double dyi = __dsub_rn(yi, ybi);
+      yb[i] = ybi;
+      gdy[i] = dyi;
+      s17[2] = __dadd_rn(s17[2], sq(dyi));                       // dy2
+      s17[3] = __dadd_rn(s17[3], sq(__dsub_rn(ybi, ay[i])));     // bar_dy2
+      oy[i] = term_orig ? __dmul_rn(ybi, __ddiv_rn(cf, rs[i])) : ybi;
+    }
+    __syncthreads();
+    // merit terms (core.py:191-197): A^T dy
+    for (int j = tid; j < n; j += kBT) {
+      double a = 0.0;
+      for (int e = atrp[j]; e < atrp[j + 1]; ++e) a = __dadd_rn(a, __dmul_rn(atv[e], gdy[atci[e]]));
+      const double dx = __dsub_rn(x[j], xb[j]);
+      s17[4] = __dadd_rn(s17[4], sq(__dadd_rn(dx, __dmul_rn(sigma, a))));   // sh2
+      s17[5] = __dadd_rn(s17[5], sq(a));                                    // aty2
+    }
+    double s11[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    kkt(s11);
+#pragma unroll
+    for (int q = 0; q < 11; ++q) s17[6 + q] = s11[q];
+    bsum<17>(s17, red);
+#pragma unroll
+    for (int q = 0; q < 11; ++q) s11[q] = s17[6 + q];
+    kkt_finish(s11);
+    have_ckpt = 1;
+    if (kk[5] <= C.tol && kk[1] <= C.tol && kk[3] <= C.tol) {
+      status = 0;
+    } else if (k >= C.max_iter) {
+      status = 1;
+    } else if (C.time_limit < INFINITY && (double)(gtimer() - t_start) * 1e-9 >= C.time_limit) {
+      status = 2;
+    } else if (C.uses_restarts) {
+      double q = s17[4] / sigma;
+      const double t1 = __dsub_rn(__dmul_rn(lamv, s17[2]), s17[5]);
+      q = __dadd_rn(q, __dmul_rn(sigma, t1));
+      const double scale = sigma * lamv * s17[2] + s17[1] / sigma;
+      if (q < -1e-9 * fmax(scale, 1e-300)) merit_neg = 1;
+      const double merit = 2.0 * sqrt(fmax(q, 0.0));
+      if (!have_first) {
+        have_first = true;
+        merit_first = merit;
+        merit_prev = INFINITY;
+      }
+      int kind = -1;                              // check_restart (driver.py:238-248)
+      if (merit <= C.a1 * merit_first) kind = 0;
+      else if (merit <= C.a2 * merit_first && merit > merit_prev) kind = 1;
+      else if ((double)t >= C.a3 * (double)k) kind = 2;
+      if (kind >= 0) {
+        double sigma_next = sigma;
+        if (C.updates_sigma) {                    // sigma_update (driver.py:251-278)
+          const double dxn = sqrt(s17[0]);
+          const double dyn = sqrt(lamv) * sqrt(s17[3]);
+          bool ok = 1e-16 < dxn && dxn < 1e12 && 1e-16 < dyn && dyn < 1e12;
+          if (ok) {
+            const double ep = kk[1], ed = kk[3];
+            if (ep == 0.0) {
+              ok = ed == 0.0;
+            } else {
+              const double ratio = ed / ep;
+              ok = 1e-8 < ratio && ratio < 1e8;
+            }
+          }
+          sigma_next = ok ? dxn / dyn : 1.0;
+        }
+        if (tid == 0 && nlog < C.max_log) {
+          hpr_restart_rec &rec = O.log[(long long)lp * C.max_log + nlog];
+          rec.outer_index = r;
+          rec.trigger = kind;
+          rec.tau = t;
+          rec.sigma_next = sigma_next;
+          rec.merit = merit;
+        }
+        ++nlog;
+        for (int i = tid; i < m; i += kBT) y[i] = ay[i] = yb[i];   // driver.py:363-364
+        for (int j = tid; j < n; j += kBT) x[j] = ax[j] = xb[j];
+        __syncthreads();
+        sigma = sigma_next;
+        ++r;
+        t = 0;
+        have_first = false;
+        merit_prev = INFINITY;
+      } else {
+        merit_prev = merit;
+      }
+    }
+  }
+
+  // ---- finish (driver.py:374-391) ----
+  if (!have_ckpt) {     // breakdown before the first checkpoint: the origin
+    for (int i = tid; i < m; i += kBT) oy[i] = 0.0;
+    for (int j = tid; j < n; j += kBT) {
+      oz[j] = 0.0;
+      ox[j] = np_clip(0.0, term_orig ? l0[j] : ls[j], term_orig ? u0[j] : us[j]);
+    }
+    __syncthreads();
+    double s11[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    kkt(s11);
+    bsum<11>(s11, red);
+    kkt_finish(s11);
+  }
+  if (!term_orig) {     // unscale + clip (driver.py:382-386)
+    for (int i = tid; i < m; i += kBT) oy[i] = __dmul_rn(oy[i], __ddiv_rn(cf, rs[i]));
+    for (int j = tid; j < n; j += kBT) {
+      const double cj = csc[j];
+      ox[j] = np_clip(__dmul_rn(ox[j], __ddiv_rn(bf, cj)), l0[j], u0[j]);
+      oz[j] = __dmul_rn(oz[j], __dmul_rn(cf, cj));
+    }
+    __syncthreads();
+  }
+  // objectives of the solution on the original problem (driver.py:388-391)
+  double f[6] = {0, 0, 0, 0, 0, 0};     // cx by lz uz nlo nup
+  for (int i = tid; i < m; i += kBT) f[1] = __dadd_rn(f[1], __dmul_rn(b0[i], oy[i]));
+  for (int j = tid; j < n; j += kBT) {
+    const double zj = oz[j];
+    f[0] = __dadd_rn(f[0], __dmul_rn(c0v[j], ox[j]));
+    if (zj > 0.0 && isfinite(l0[j])) {
+      f[2] = __dadd_rn(f[2], __dmul_rn(l0[j], zj));
+      f[4] += 1.0;
+    } else if (zj < 0.0 && isfinite(u0[j])) {
+      f[3] = __dadd_rn(f[3], __dmul_rn(u0[j], zj));
+      f[5] += 1.0;
+    }
+  }
+  bsum<6>(f, red);
+  if (tid == 0) {
+    double pobj = f[0] + oc;
+    double dobj = f[1];
+    if (f[4] != 0.0) dobj += f[2];
+    if (f[5] != 0.0) dobj += f[3];
+    dobj += oc;
+    if (P.obj_neg[lp]) {
+      pobj = -pobj;
+      dobj = -dobj;
+    }
+    hpr_batch_result &R = O.res[lp];
+    R.status = status;
+    R.restarts = r;
+    R.iterations = k;
+    R.power_iterations = piters;
+    R.power_converged = pconv;
+    R.dual_clamped = (int)clamped;
+    R.n_log = nlog;
+    R.merit_negative = merit_neg;
+    R.power_failed = start == -2;
+    R.primal_objective = pobj;
+    R.dual_objective = dobj;
+    for (int q = 0; q < 9; ++q) R.kkt[q] = kk[q];
+    R.sigma_final = sigma;
+    R.lambda_estimate = lamv;
+    R.lambda_raw = lam_raw;
+    R.b_factor = bf;
+    R.c_factor = cf;
+    R.device_seconds = (double)(gtimer() - t_start) * 1e-9;
+  }
+}
+
+// ---- transpose of the whole batch (block-diagonal matrix) ----
+__global__ void k_batch_keys(const int64_t *row_off, const int64_t *col_off, const int64_t *nz_off,
+                             const int *rp, const int *ci, int *key, int *rowl, int count) {
+  const int lp = blockIdx.x;
+  if (lp >= count) return;
+  const long long r0 = row_off[lp], c0 = col_off[lp], z0 = nz_off[lp];
+  const int m = (int)(row_off[lp + 1] - r0);
+  const int *lrp = rp + r0 + lp;
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    for (int e = lrp[i]; e < lrp[i + 1]; ++e) {
+      key[z0 + e] = (int)(c0 + ci[z0 + e]);
+      rowl[z0 + e] = i;
+    }
+}
+__global__ void k_batch_gather(const int *perm, const int *rowl, const double *val, int *cit,
+                               double *valt, long long nnz) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int p = perm[k];
+    cit[k] = rowl[p];
+    valt[k] = val[p];
+  }
+}
+// grpt[c0 + lp + j] = global position of column j of LP lp (n + 1 entries per LP)
+__global__ void k_batch_rpt(const int64_t *col_off, const int *gcount_rpt, int *grpt, int count) {
+  const int lp = blockIdx.x;
+  if (lp >= count) return;
+  const long long c0 = col_off[lp];
+  const int n = (int)(col_off[lp + 1] - c0);
+  for (int j = threadIdx.x; j <= n; j += blockDim.x) grpt[c0 + lp + j] = gcount_rpt[c0 + j];
+}
+
+}  // namespace batch
+}  // namespace hpr
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+
+struct BatchWs {
+  size_t key, rowl, iota, perm, skey, gcrpt, grpt, cit, valt, dy, cub, cub_bytes, total;
+};
+
+int batch_layout(const hpr_batch_problem *p, BatchWs *L) {
+  const long long nnz = p->total_nnz, nr = p->total_rows, nc = p->total_cols;
+  size_t cb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, cb, (const int *)nullptr, (int *)nullptr,
+                                     (const int *)nullptr, (int *)nullptr, (int)std::max(nnz, 1LL),
+                                     0, 32));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 16), 256);
+    return o;
+  };
+  L->key = take(4 * nnz);
+  L->rowl = take(4 * nnz);
+  L->iota = take(4 * nnz);
+  L->perm = take(4 * nnz);
+  L->skey = take(4 * nnz);
+  L->gcrpt = take(4 * (nc + 1));
+  L->grpt = take(4 * (nc + p->count));
+  L->cit = take(4 * nnz);
+  L->valt = take(8 * nnz);
+  L->dy = take(8 * nr);
+  L->cub_bytes = cb;
+  L->cub = take(cb);
+  L->total = off;
+  return HPR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpr_batch_smem_bytes(int32_t max_m, int32_t max_n, int64_t max_nnz, size_t *bytes) {
+  if (!bytes || max_m < 1 || max_n < 1 || max_nnz < 0) return fail(HPR_EINVAL, "bad argument");
+  *bytes = hpr::batch::smem_bytes(max_m, max_n, max_nnz);
+  return HPR_OK;
+}
+
+int hpr_batch_workspace_bytes(const hpr_batch_problem *p, size_t *bytes) {
+  if (!p || !bytes) return fail(HPR_EINVAL, "null argument");
+  if (p->count < 1 || p->total_nnz < 0 || p->total_nnz >= INT_MAX || p->total_cols >= INT_MAX)
+    return fail(HPR_EINVAL, "invalid batch dims");
+  BatchWs L;
+  int rc = batch_layout(p, &L);
+  if (rc) return rc;
+  *bytes = L.total;
+  return HPR_OK;
+}
+
+int hpr_batch_solve(const hpr_batch_problem *p, const hpr_batch_config *cfg, void *workspace,
+                    size_t ws_bytes, hpr_batch_result *results, hpr_restart_rec *log,
+                    double *x, double *y, double *z, int device, void *stream) {
+  using namespace hpr::batch;
+  if (!p || !cfg || !workspace || !results || !x || !y || !z) return fail(HPR_EINVAL, "null argument");
+  if (cfg->max_log > 0 && !log) return fail(HPR_EINVAL, "null restart log");
+  if (cfg->variant < 0 || cfg->variant > 3) return fail(HPR_EINVAL, "bad variant");
+  if (cfg->check_interval < 1 || !(cfg->tolerance > 0.0)) return fail(HPR_EINVAL, "bad config");
+  BatchWs L;
+  int rc = batch_layout(p, &L);
+  if (rc) return rc;
+  if (ws_bytes < L.total) return fail(HPR_EINVAL, "batch workspace too small");
+  const size_t smem = smem_bytes(p->max_m, p->max_n, p->max_nnz);
+  int dev_smem = 0;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  if (smem > (size_t)dev_smem)
+    return fail(HPR_EINVAL, "an LP of the batch does not fit in one CTA's shared memory (" +
+                                std::to_string(smem) + " > " + std::to_string(dev_smem) + " bytes)");
+  cudaStream_t s = (cudaStream_t)stream;
+  char *ws = (char *)workspace;
+  int *key = (int *)(ws + L.key), *rowl = (int *)(ws + L.rowl), *iota = (int *)(ws + L.iota);
+  int *perm = (int *)(ws + L.perm), *skey = (int *)(ws + L.skey);
+  int *gcrpt = (int *)(ws + L.gcrpt), *grpt = (int *)(ws + L.grpt), *cit = (int *)(ws + L.cit);
+  double *valt = (double *)(ws + L.valt), *dy = (double *)(ws + L.dy);
+  const long long nnz = p->total_nnz;
+  const int nc = (int)p->total_cols;
+  const int count = (int)p->count;
+  // stable transpose of the block-diagonal batch matrix: sort by global column,
+  // rows stay ascending inside a column (csr_matrix(A.T) order, sparse.py:98-100)
+  if (nnz > 0) {
+    k_batch_keys<<<count, 128, 0, s>>>(p->row_off, p->col_off, p->nz_off, p->rp, p->ci, key, rowl,
+                                       count);
+    k_iota<<<grid_for(nnz), 256, 0, s>>>(iota, nnz);
+    CKL();
+    int end_bit = 1;
+    while ((1LL << end_bit) < nc) ++end_bit;
+    size_t tb = L.cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(ws + L.cub, tb, key, skey, iota, perm, (int)nnz, 0, end_bit, s));
+    k_col_count<<<grid_for(nnz), 256, 0, s>>>(skey, nnz, nc, gcrpt);
+    k_batch_gather<<<grid_for(nnz), 256, 0, s>>>(perm, rowl, p->val, cit, valt, nnz);
+    CKL();
+  } else {
+    k_fill_empty_rpt<<<grid_for(nc + 1), 256, 0, s>>>(gcrpt, nc);
+    CKL();
+  }
+  k_batch_rpt<<<count, 128, 0, s>>>(p->col_off, gcrpt, grpt, count);
+  CKL();
+  Prob P{p->row_off, p->col_off, p->nz_off, p->m1, p->rp, p->ci, p->val, grpt, cit, valt,
+         p->b, p->c, p->lower, p->upper, p->obj_const, p->obj_neg};
+  Cfg C{};
+  C.tol = cfg->tolerance;
+  C.time_limit = cfg->time_limit_seconds;
+  C.a1 = cfg->alpha1;
+  C.a2 = cfg->alpha2;
+  C.a3 = cfg->alpha3;
+  C.sigma0 = cfg->sigma0;
+  C.power_tol = cfg->power_tol;
+  C.max_iter = cfg->max_iterations;
+  C.check_interval = cfg->check_interval;
+  // variant codes of the batch config: 0 DR, 1 HDR-fixed, 2 HDR, 3 HPR
+  C.variant = cfg->variant == 0 ? 0 : (cfg->variant == 3 ? 2 : 1);
+  C.uses_restarts = cfg->variant != 0;
+  C.updates_sigma = cfg->variant >= 2;
+  C.ruiz = cfg->ruiz_iters;
+  C.pc = cfg->pock_chambolle;
+  C.bc = cfg->bc_normalize;
+  C.power_max = cfg->power_max_iters;
+  C.term_original = cfg->term_original;
+  C.max_log = cfg->max_log;
+  Out O{results, log, x, y, z, dy};
+  CK(cudaFuncSetAttribute(k_batch_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_batch_solve<<<count, kBT, smem, s>>>(P, C, O);
+  CKL();
+  return HPR_OK;
+}
+
+}  // extern "C"

@@ -61,13 +61,13 @@ int64_t windows_of(int64_t nrows) { return (nrows + kWindow - 1) / kWindow; }
 
 // per-matrix plan arrays in the main workspace
 struct PlanOff {
-  size_t slice_row, slice_slots, slice_ptr, long_flag, long_rows, nsel;
+  size_t slice_row, slice_len, slice_slots, slice_ptr, long_flag, long_rows, nsel;
 };
 
 struct Layout {
   PlanOff pa, pat;
   size_t keys_out, iota, row_of, cub_tmp, cub_bytes, dvec_m, dvec_n, part, part_count, params,
-      pow, results, fac, total;
+      pow, results, fac, flags, total;
 };
 
 int cub_temp_bytes(const hpr_dims &d, size_t *bytes) {
@@ -97,6 +97,7 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
     const int64_t nw = windows_of(nrows);
     const int64_t ns = nw * (kWindow / kSlice);
     p.slice_row = take(sizeof(int) * nw * kWindow);
+    p.slice_len = take(sizeof(unsigned short) * nw * kWindow);
     p.slice_slots = take(sizeof(int) * (ns + 1));
     p.slice_ptr = take(sizeof(int) * (ns + 1));
     p.long_flag = take(sizeof(int) * nrows);
@@ -122,6 +123,7 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
   L.pow = take(sizeof(PowState));
   L.results = take(sizeof(double) * 64);
   L.fac = take(sizeof(double) * 2);
+  L.flags = take(sizeof(unsigned int) * 4);
   L.total = off;
   return L;
 }
@@ -137,6 +139,7 @@ int grid_for(int64_t n, int threads = 256, int max_blocks = 148 * 16) {
 struct Sell {
   int nrows = 0, nslices = 0, nlong = 0;
   long long slots = 0;
+  unsigned short *slice_len = nullptr;
   int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *long_flag = nullptr,
       *long_rows = nullptr, *nsel = nullptr;
   int *ci = nullptr, *pos = nullptr;
@@ -158,6 +161,9 @@ struct hpr_ctx {
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
   PowState *pow = nullptr;
+  unsigned int *flags = nullptr;
+  int bounds_uniform = 0;          // see EpiXIter
+  double lo_u = 0.0, up_u = 0.0;
   double *h_results = nullptr;       // pinned
   IterParams *h_params = nullptr;    // pinned
   PowState *h_pow = nullptr;         // pinned
@@ -168,7 +174,7 @@ struct hpr_ctx {
   long long launches = 0;
 
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
-    return SellMat{S.slice_ptr, S.slice_row, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
+    return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
                    S.long_rows, S.nslices, S.nlong};
   }
   SellMat mat_a(bool scaled) const {
@@ -227,6 +233,7 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) 
   const int nw = (int)windows_of(nrows);
   S.nslices = nw * (kWindow / kSlice);
   S.slice_row = (int *)(c->ws + po.slice_row);
+  S.slice_len = (unsigned short *)(c->ws + po.slice_len);
   S.slice_slots = (int *)(c->ws + po.slice_slots);
   S.slice_ptr = (int *)(c->ws + po.slice_ptr);
   S.long_flag = (int *)(c->ws + po.long_flag);
@@ -234,7 +241,8 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) 
   S.nsel = (int *)(c->ws + po.nsel);
   cudaStream_t s = c->stream;
   CK(cudaMemsetAsync(S.slice_slots + S.nslices, 0, sizeof(int), s));
-  k_sell_plan<<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_slots, S.long_flag);
+  k_sell_plan<<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots,
+                                     S.long_flag);
   CKL();
   size_t tb = c->L.cub_bytes;
   CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, S.slice_slots, S.slice_ptr,
@@ -465,6 +473,7 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
   c->dvec_n = (double *)(c->ws + L.dvec_n);
   c->params = (IterParams *)(c->ws + L.params);
   c->pow = (PowState *)(c->ws + L.pow);
+  c->flags = (unsigned int *)(c->ws + L.flags);
   for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
   c->inner_graphs.clear();
   if (c->pow_graph) {
@@ -624,10 +633,30 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
                         RedSeg{P.misc + 2 * kSumsqBlocks, nbm, R_SUMSQ2},
                         RedSeg{P.misc + 3 * kSumsqBlocks, nbn, R_SUMSQ3}});
   if (rc) return rc;
+  // uniform scaled bounds (x-phase reads a scalar instead of the vector)
+  const unsigned int ones[2] = {1u, 1u};
+  CK(cudaMemcpyAsync(c->flags, ones, sizeof(ones), cudaMemcpyHostToDevice, s));
+  k_uniform<<<grid_for(n), 256, 0, s>>>(B.lower_s, n, c->flags);
+  k_uniform<<<grid_for(n), 256, 0, s>>>(B.upper_s, n, c->flags + 1);
+  CKL();
+  c->launches += 2;
+  unsigned int hfl[2];
+  double hb[2];
+  CK(cudaMemcpyAsync(hfl, c->flags, sizeof(hfl), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hb, B.lower_s, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hb + 1, B.upper_s, sizeof(double), cudaMemcpyDeviceToHost, s));
   double fac[2];
   CK(cudaMemcpyAsync(fac, c->fac, sizeof(fac), cudaMemcpyDeviceToHost, s));
   rc = fetch_results(c);
   if (rc) return rc;
+  const int bu = (hfl[0] ? 1 : 0) | (hfl[1] ? 2 : 0);
+  if (bu != c->bounds_uniform || (bu && (std::memcmp(&hb[0], &c->lo_u, 8) || std::memcmp(&hb[1], &c->up_u, 8)))) {
+    for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
+    c->inner_graphs.clear();
+  }
+  c->bounds_uniform = bu;
+  c->lo_u = hb[0];
+  c->up_u = hb[1];
   if (out) {
     out->b_factor = fac[0];
     out->c_factor = fac[1];
@@ -771,6 +800,9 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     ex.c = B.c_s;
     ex.lo = B.lower_s;
     ex.up = B.upper_s;
+    ex.bounds_uniform = c->bounds_uniform;
+    ex.lo_u = c->lo_u;
+    ex.up_u = c->up_u;
     ex.anc = B.anc_x;
     ex.x = B.x;
     ex.w = B.w;
@@ -963,3 +995,4 @@ int hpr_last_times(hpr_ctx *c, double *inner_ms, double *ckpt_ms) {
 }  // extern "C"
 
 #include "hpr_rowblock.cuh"
+#include "hpr_batch.cuh"

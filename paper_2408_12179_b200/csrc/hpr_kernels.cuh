@@ -66,6 +66,7 @@ __device__ __forceinline__ int ld_stream(const int *ptr, uint64_t pol) {
 struct SellMat {
   const int *slice_ptr;    // nslices + 1 (slot offsets)
   const int *slice_row;    // nslices * 32: row of (slice, lane) or -1
+  const unsigned short *slice_len;  // nslices * 32: that row's length (0 for padding)
   const int *ci;           // slots
   const double *val;       // slots
   const int *rp;           // CSR row pointers
@@ -151,14 +152,13 @@ template <class Epi>
 __device__ __forceinline__ void sell_slice(const SellMat &M, int s, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
+  // row, length and the slice's slot range are independent loads (no chain
+  // through the CSR row pointers)
   const int row = M.slice_row[s * kSlice + lane];
+  const int len = M.slice_len[s * kSlice + lane];
   const int base = M.slice_ptr[s];
   const int slen = (M.slice_ptr[s + 1] - base) / kSlice;
-  int len = 0;
-  if (row >= 0) {
-    len = M.rp[row + 1] - M.rp[row];
-    epi.prefetch(row);
-  }
+  if (row >= 0) epi.prefetch(row);
   const int *cp = M.ci + base + lane;
   const double *vp = M.val + base + lane;
   double sum = 0.0;
@@ -295,6 +295,8 @@ struct EpiXIter {
   double *x, *w;
   IterParams *P;
   int step;
+  int bounds_uniform;        // bit 0: every lower bound equals lo_u, bit 1: upper / up_u
+  double lo_u, up_u;
   double sigma, wa, wn, xj, cj, lj, uj, aj;
   int variant;
   __device__ bool enter() {
@@ -306,8 +308,8 @@ struct EpiXIter {
   __device__ void prefetch(int j) {
     xj = x[j];
     cj = c[j];
-    lj = lo[j];
-    uj = up[j];
+    lj = (bounds_uniform & 1) ? lo_u : lo[j];
+    uj = (bounds_uniform & 2) ? up_u : up[j];
     aj = variant ? anc[j] : 0.0;
   }
   __device__ void finish(int j, double aty, double *) {
@@ -659,8 +661,8 @@ __global__ void k_gather_t(const int *perm, const int *row_of, const double *val
 // index asc); long rows and padding go last with row = -1.  Writes slice_row
 // and the slot count of each slice (32 * longest row in it).
 __global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows, int sort_rows,
-                                                       int *slice_row, int *slice_slots,
-                                                       int *long_flag) {
+                                                       int *slice_row, unsigned short *slice_len,
+                                                       int *slice_slots, int *long_flag) {
   __shared__ int key[kWindow];
   __shared__ int skey[kWindow];
   const int t = threadIdx.x;
@@ -683,6 +685,7 @@ __global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows,
   }
   skey[rank] = k;
   slice_row[blockIdx.x * kWindow + rank] = k >= 0 ? r : -1;
+  slice_len[blockIdx.x * kWindow + rank] = (unsigned short)(k >= 0 ? k : 0);
   __syncthreads();
   if (t < kWindow / kSlice) {
     int mx = 0;
@@ -841,6 +844,17 @@ __global__ void k_unscale(const double *sy, const double *sz, const double *sx, 
     ox[j] = np_clip(__dmul_rn(sx[j], __ddiv_rn(bf, c)), lo0[j], up0[j]);
     oz[j] = __dmul_rn(sz[j], __dmul_rn(cf, c));
   }
+}
+
+// flag[0] &= (a[j] is bitwise a[0] for every j): uniform bound vectors (e.g.
+// x >= 0) are then passed to the x-phase as a scalar instead of streamed
+__global__ void k_uniform(const double *a, long long n, unsigned int *flag) {
+  const unsigned long long a0 = __double_as_longlong(a[0]);
+  bool same = true;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    same &= (unsigned long long)__double_as_longlong(a[i]) == a0;
+  if (!__all_sync(0xffffffffu, same) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0u);
 }
 
 __global__ void k_reset_params(IterParams *P) {

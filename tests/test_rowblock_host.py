@@ -134,3 +134,31 @@ def test_partitioned_iteration_gloo_world2():
     ref = np.concatenate([st.y, st.x])
     got = np.concatenate([y, x])
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_batch_shard_bounds_cover():
+    from paper_2408_12179_b200.batch import shard_bounds
+    for count in (1, 7, 4096):
+        for world in (1, 2, 3, 8):
+            if count < world:
+                continue
+            spans = [shard_bounds(count, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == count
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [h - l for l, h in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_batch_packing_offsets():
+    from paper_2408_12179_b200.batch import PackedBatch
+    probs = [generate_known_solution_lp(10_000 + i, 5, 6, 20, 0.3)[0] for i in range(3)]
+    pk = PackedBatch(probs)
+    a = pk.arrays
+    assert pk.count == 3 and a["row_off"][-1] == 33 and a["col_off"][-1] == 60
+    for i, p in enumerate(probs):
+        ro, ci, v, m, n, m1 = stacked_arrays(p)
+        r0 = pk.row_off[i]
+        assert np.array_equal(a["rp"][r0 + i:r0 + i + m + 1], ro)
+        z0, z1 = pk.nz_off[i], pk.nz_off[i + 1]
+        assert np.array_equal(a["ci"][z0:z1], ci) and np.array_equal(a["val"][z0:z1], v)
+        assert a["m1"][i] == m1
