@@ -1,23 +1,35 @@
 #!/usr/bin/env python
-"""Benchmark of the HPR-LP iteration loop on B200 (contract: see DESIGN.md §Measurement).
+"""Benchmark of the HPR-LP iteration loop on B200 (contract: DESIGN.md §6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1|c3|c3-lite]
+                    [--config c2|c1|c3|c3-lite|c4|c5]
 
-A step is one full solve of the configuration to its tolerance (C2: 1e-8)
-starting from a problem already resident in HBM (setup = transpose/tiling,
-scaling and power method are inside the step).  ``value`` = HPR iterations per
-second over the K timed steps (sum over ranks; each rank solves its own replica
--- the C2 path fits one GPU, so N > 1 is weak scaling of independent solves).
-``e2e`` = the same metric through the public ``solve()`` call on a host
-problem, with the pinned H2D upload and the D2H of the solution inside the
-timed region.  ``roofline`` is the fused x-phase + y-phase iteration pair
-against the measured HBM copy bandwidth, algorithmic bytes per iteration
-B_iter = 24 nnz + 4 (m + n + 2) + 8 (5 m + 8 n).
+c1/c2/c3 (default c2 = BASELINE configs[1], the headline): a step is one full
+solve to tolerance (C2: 1e-8) from a problem already resident in HBM (setup =
+transpose/layout, scaling and power method are inside the step).  ``value`` =
+HPR iterations per second; at N > 1 every rank solves its own replica
+(independent objects, no collective: C2 fits one GPU) -- weak scaling.
 
-``--impl reference`` times the CPU oracle port (oracle/, the reference's
-algorithm restated with sequential-order C kernels; OpenMP over all host
-cores) on the same instance: each step is one 150-iteration interval.
+c4: the row-block partitioned path: each rank owns
+``--c4-rows`` rows x 100 nnz of a planted LP with n = 20M columns, generated
+per rank; the A^T y partials are reduce-scattered and w all-gathered over
+NCCL every iteration.  A step = one 150-iteration interval + checkpoint.
+Weak scaling (rows per rank fixed; N = 8 is C4's 1e9 nnz).
+
+c5: a batch of 4096 LPs (m=500, n=1000, nnz=5000), one whole solve per CTA,
+sharded across ranks (no collective).  A step = the whole shard solved to
+1e-8.  ``value`` = LP-iterations per second summed over ranks.
+
+``e2e`` = the same metric through the public API (``solve`` /
+``solve_batch`` / ``solve_distributed``) on host data, with the H2D upload and
+the D2H of the solution inside the timed region.  ``roofline`` is the fused
+x-phase + y-phase iteration pair against the measured HBM copy bandwidth,
+B_iter = 24 nnz + 4 (m + n + 2) + 8 (5 m + 8 n) bytes per iteration.
+
+``--impl reference`` times the CPU oracle port (oracle/: the reference
+algorithm with sequential-order C kernels; OpenMP over all host cores, or a
+process pool for c5) on the same instance -- the reference is pure Python, so
+there is no compiled oracle/_ref.
 """
 
 from __future__ import annotations
@@ -39,11 +51,27 @@ sys.path.insert(0, ROOT)
 CONFIG_NAMES = {"c1": "C1: known-solution LP m=1000 n=2000 nnz=20000, tol 1e-4",
                 "c2": "C2: known-solution LP m=100000 n=200000 nnz=5000000, tol 1e-8",
                 "c3": "C3: multicommodity flow V=2^18 E=2^20 K=32 (nnz ~1.0e8), tol 1e-8",
-                "c3-lite": "C3-lite: multicommodity flow V=2^10 K=8, tol 1e-8"}
+                "c3-lite": "C3-lite: multicommodity flow V=2^10 K=8, tol 1e-8",
+                "c4": "C4: planted LP row-block partitioned over N GPUs, n=2e7, 100 nnz/row",
+                "c5": "C5: batch of 4096 LPs m=500 n=1000 nnz=5000, one per CTA, tol 1e-8"}
+C4_N = 20_000_000
+C4_PER_ROW = 100
+C5_COUNT = 4096
 
 
 def b_iter(m, n, nnz):
     return 24 * nnz + 4 * (m + n + 2) + 8 * (5 * m + 8 * n)
+
+
+def load_traffic(config):
+    """ncu DRAM bytes (read + write) of the x-phase + y-phase pair per iteration,
+    from the committed capture summary (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        v = d.get(config)
+        return None if v is None else float(v["bytes_per_iteration"])
+    return None
 
 
 def load_peaks():
@@ -113,42 +141,116 @@ def make_instance(name):
     return config_instance(name)
 
 
-def cpu_baseline_sample(prob, tol, iters=300):
-    """Oracle (C kernels, all host threads) on the same instance: setup once,
-    then `iters` HPR iterations timed; it/s."""
+def c5_problems(lo, hi):
+    from paper_2408_12179_b200.generators import generate_known_solution_lp
+    return [generate_known_solution_lp(10_000 + i, 250, 250, 1000, 0.01)[0] for i in range(lo, hi)]
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline (the oracle port; test infrastructure)
+# ---------------------------------------------------------------------------
+
+def _oracle_setup(prob):
     from oracle import hprlp_oracle as O
     lib = O.load_clib()
-    threads = lib.orc_set_threads(os.cpu_count() or 1) if lib is not None else 1
+    threads = lib.orc_set_threads(cpu_threads()) if lib is not None else 1
     lp = O.OracleLP.from_problem(prob)
     scaled, _ = O.scale_lp(lp)
     est = O.power_lambda(scaled)
     st = O.State(y=np.zeros(scaled.m), x=np.zeros(scaled.n), ay=np.zeros(scaled.m),
                  ax=np.zeros(scaled.n), sigma=1.0, lam=est.value)
+    return O, scaled, st, threads
+
+
+def cpu_baseline_sample(prob, iters=300):
+    """Oracle C kernels (all host threads) on the same instance: setup once,
+    then ``iters`` HPR iterations timed; it/s."""
+    O, scaled, st, threads = _oracle_setup(prob)
     O.iterate_once(st, scaled)  # warm
     t0 = time.perf_counter()
     for _ in range(iters):
         O.iterate_once(st, scaled)
     dt = time.perf_counter() - t0
-    return {"value": iters / dt, "unit": "it/s", "cores": threads,
-            "kind": "port" if lib is None else "port",
+    return {"value": iters / dt, "unit": "it/s", "cores": threads, "kind": "port",
             "sample": f"{iters} HPR iterations of the same instance (oracle C kernels, "
                       f"sequential per-row sums, OpenMP {threads} threads), setup excluded"}
+
+
+def _c5_worker(i):
+    from oracle import hprlp_oracle as O
+    lib = O.load_clib()
+    if lib is not None:
+        lib.orc_set_threads(1)
+    prob = c5_problems(i, i + 1)[0]
+    t0 = time.perf_counter()
+    rep = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(tolerance=1e-8))
+    return rep["iterations"], time.perf_counter() - t0
+
+
+def c5_cpu_sample(count):
+    """``count`` C5 LPs solved by the oracle in a process pool over all cores;
+    LP-iterations per second of wall time."""
+    import multiprocessing as mp
+    cores = cpu_threads()
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(min(cores, count)) as pool:
+        out = pool.map(_c5_worker, range(count))
+    dt = time.perf_counter() - t0
+    its = sum(o[0] for o in out)
+    return {"value": its / dt, "unit": "LP-it/s", "cores": min(cores, count), "kind": "port",
+            "sample": f"{count} of the 4096 C5 LPs solved to 1e-8 by the oracle (one LP per "
+                      f"process, {min(cores, count)} processes), wall time incl. setup"}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import hprlp_oracle as O
-    prob, tol = make_instance(args.config)
-    lib = O.load_clib()
-    threads = lib.orc_set_threads(os.cpu_count() or 1) if lib is not None else 1
-    lp = O.OracleLP.from_problem(prob)
-    scaled, _ = O.scale_lp(lp)
-    est = O.power_lambda(scaled)
-    st = O.State(y=np.zeros(scaled.m), x=np.zeros(scaled.n), ay=np.zeros(scaled.m),
-                 ax=np.zeros(scaled.n), sigma=1.0, lam=est.value)
-    interval = 150
+    base = {"metric": "hpr_iterations_per_sec", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference"}
+    if args.config == "c5":
+        cnt = max(cpu_threads(), 16)
+        vals = []
+        for _ in range(args.steps):
+            vals.append(c5_cpu_sample(cnt))
+        val = statistics.median(v["value"] for v in vals)
+        cb = dict(vals[0], value=val)
+        line = dict(base, metric="hpr_lp_iterations_per_sec", value=val, unit="LP-it/s",
+                    ms_per_step=None,
+                    config={"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
+                            "step": cb["sample"]},
+                    cpu_baseline=cb,
+                    e2e={"value": val, "unit": "LP-it/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+    if args.config == "c4":
+        from paper_2408_12179_b200.generators import generate_planted_block
+        from paper_2408_12179_b200 import LpProblem, SparseMatrix
+        rows = args.c4_rows
+        m1 = rows // 2
+        rp, ci, va, b, ys, m1l, (lo, up, xs, zs), cpart = generate_planted_block(
+            4, m1, rows - m1, C4_N, C4_PER_ROW, 0, rows)
+        c = cpart + zs
+        prob = LpProblem(a_eq=SparseMatrix.from_csr_arrays(rp[:m1 + 1], ci[:rp[m1]], va[:rp[m1]], m1, C4_N),
+                         a_ineq=SparseMatrix.from_csr_arrays(rp[m1:] - rp[m1], ci[rp[m1]:], va[rp[m1]:],
+                                                             rows - m1, C4_N),
+                         b_eq=b[:m1], b_ineq=b[m1:], c=c, lower=lo, upper=up)
+        interval = 2
+        tol = 1e-8
+    else:
+        prob, tol = make_instance(args.config)
+        interval = 150
+    O, scaled, st, threads = _oracle_setup(prob)
 
     def step():
         for _ in range(interval):
@@ -161,32 +263,62 @@ def run_reference(args):
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    its = interval * args.steps
-    val = its / dt
-    line = {"metric": "hpr_iterations_per_sec", "value": val, "unit": "it/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": CONFIG_NAMES[args.config], "tolerance": tol,
-                       "step": f"{interval} HPR iterations + 1 half step (oracle port)"},
-            "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} x {interval} iterations"},
-            "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    val = interval * args.steps / dt
+    line = dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
+                config={"workload": CONFIG_NAMES[args.config], "tolerance": tol,
+                        "step": f"{interval} HPR iterations + 1 half step (oracle port)"},
+                cpu_baseline={"value": val, "unit": "it/s", "cores": threads, "kind": "port",
+                              "sample": f"{args.steps} x {interval} iterations + half step"},
+                e2e={"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def _dist_init(ws, local):
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist
+    return None
+
+
+def _max_sum(dist, local, t_local, count):
+    """(max over ranks of t_local, sum over ranks of count)."""
+    if dist is None:
+        return t_local, count
+    import torch
+    tt = torch.tensor([t_local, float(count)], dtype=torch.float64, device=f"cuda:{local}")
+    tmax = tt.clone()
+    dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+    dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+    return float(tmax[0]), float(tt[1])
+
+
+def _finish(dist, line, rank):
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_ours(args):
     import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = _dist_init(ws, local)
+    if args.config == "c5":
+        return run_c5(args, dist, ws, rank, local)
+    if args.config == "c4":
+        return run_c4(args, dist, ws, rank, local)
     import paper_2408_12179_b200 as P
     from paper_2408_12179_b200.device import DeviceLP
 
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prob, tol = make_instance(args.config)
     cfg = P.SolverConfig(tolerance=tol)
     dev = DeviceLP(prob, device=local)
@@ -199,13 +331,13 @@ def run_ours(args):
             dist.barrier()
             torch.cuda.synchronize()
 
-    # warmup (also builds the graphs)
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):             # also builds the graphs
         P.solve(prob, cfg, dev=dev)
     sample_clocks = ClockSampler(local)
     total_ms = 0.0
     its_total = 0
     iter_s_total = 0.0
+    pair_ms = []
     reps = []
     l0 = dev.launch_count()
     barrier()
@@ -225,15 +357,7 @@ def run_ours(args):
             reps.append(rep)
     barrier()
     launches = dev.launch_count() - l0
-    t_local = total_ms / 1e3
-    t_max = t_local
-    its_all = its_total
-    if dist is not None:
-        tt = torch.tensor([t_local, float(its_total)], dtype=torch.float64, device=f"cuda:{local}")
-        tmax = tt.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
-        t_max, its_all = float(tmax[0]), float(tt[1])
+    t_max, its_all = _max_sum(dist, local, total_ms / 1e3, its_total)
     value = its_all / t_max
 
     # e2e through the public API from host arrays (upload + solve + D2H solution)
@@ -248,11 +372,8 @@ def run_ours(args):
         e2e_its += rep.iterations
         h2d = rep.device_stats["h2d_bytes"]
         d2h = 8 * (2 * n + m)
-    e2e_val = e2e_its / e2e_t
-    if dist is not None:
-        tt = torch.tensor([e2e_val], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        e2e_val = float(tt[0])
+    t_e2e, its_e2e = _max_sum(dist, local, e2e_t, e2e_its)
+    e2e_val = its_e2e / t_e2e
 
     peak, peak_kind = load_peaks()
     bi = b_iter(m, n, nnz)
@@ -260,7 +381,7 @@ def run_ours(args):
     line = None
     if rank == 0:
         r0 = reps[-1]
-        cpu = cpu_baseline_sample(prob, tol) if ws == 1 and not args.no_cpu else None
+        cpu = cpu_baseline_sample(prob) if ws == 1 and not args.no_cpu else None
         line = {
             "metric": "hpr_iterations_per_sec", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
@@ -273,19 +394,182 @@ def run_ours(args):
                        "l2": "256 MB buffer written between timed steps (flush)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_x_iter + k_y_iter (one HPR iteration)",
-                         "bytes_per_iteration": bi, "peak_source": peak_kind},
+                         "frac": achieved / peak,
+                         "traffic": args.traffic if args.traffic is not None
+                         else load_traffic(args.config),
+                         "kernel": "k_sell<EpiXIter> + k_sell<EpiYIter> (one HPR iteration)",
+                         "bytes_per_iteration": bi, "peak_source": peak_kind,
+                         "timing": "CUDA events around each 150-iteration graph replay"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": sample_clocks.summary(),
         }
-        print(json.dumps(line), flush=True)
+    _finish(dist, line, rank)
+    return line
+
+
+def run_c5(args, dist, ws, rank, local):
+    import torch
+    import paper_2408_12179_b200 as P
+    from paper_2408_12179_b200.batch import BatchRun, PackedBatch, shard_bounds, solve_batch
+    lo, hi = shard_bounds(C5_COUNT, ws, rank)
+    probs = c5_problems(lo, hi)
+    cfg = P.SolverConfig(tolerance=1e-8)
+    run = BatchRun(PackedBatch(probs), device=local)
+    for _ in range(args.warmup):
+        run.launch(cfg)
+    run.stream.synchronize()
+    sample_clocks = ClockSampler(local)
+    total_ms, its = 0.0, 0
+    l0 = run.launches
+    with sample_clocks:
+        for _ in range(args.steps):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(run.stream)
+            run.launch(cfg)
+            ev1.record(run.stream)
+            ev1.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            reps = run.reports(cfg)
+            its += sum(r.iterations for r in reps)
+    launches = run.launches - l0
+    t_max, its_all = _max_sum(dist, local, total_ms / 1e3, its)
+    value = its_all / t_max
+    st = {}
+    for r in reps:
+        st[r.status.value] = st.get(r.status.value, 0) + 1
+    # e2e: solve_batch on host problems (pack + upload + solve + D2H of every report)
+    e2e_t, e2e_its = 0.0, 0
+    pk = PackedBatch(probs)
+    for _ in range(max(1, min(args.steps, 2))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = solve_batch(probs, cfg, device=local)
+        e2e_t += time.perf_counter() - t0
+        e2e_its += sum(r.iterations for r in reps)
+    t_e2e, its_e2e = _max_sum(dist, local, e2e_t, e2e_its)
+    line = None
+    if rank == 0:
+        cpu = c5_cpu_sample(max(cpu_threads(), 16)) if ws == 1 and not args.no_cpu else None
+        line = {
+            "metric": "hpr_lp_iterations_per_sec", "value": value, "unit": "LP-it/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
+                       "lps_per_rank": hi - lo, "lps_total": C5_COUNT,
+                       "step": "the rank's shard solved to 1e-8 in one launch (one LP per CTA)",
+                       "status": st, "l2": "inputs re-read from HBM each step (490 MB > L2)",
+                       "parallelism": f"batch sharded x{ws}" if ws > 1 else "single GPU"},
+            "roofline": None,
+            "cpu_baseline": cpu,
+            "e2e": {"value": its_e2e / t_e2e, "unit": "LP-it/s",
+                    "h2d_bytes_per_step": pk.h2d_bytes(),
+                    "d2h_bytes_per_step": 8 * int(pk.row_off[-1] + 2 * pk.col_off[-1])},
+            "gpu_launches": launches,
+            "clocks": sample_clocks.summary(),
+        }
+    _finish(dist, line, rank)
+    return line
+
+
+def c4_block(rank, ws, rows_per_rank, local, dist):
+    """This rank's rows of the weak-scaled C4 instance + the global cost vector."""
+    import torch
+    from paper_2408_12179_b200.generators import _planted_columns, generate_planted_block
+    m = rows_per_rank * ws
+    m1 = m // 2
+    cols = _planted_columns(4, C4_N)
+    r0, r1 = rank * rows_per_rank, (rank + 1) * rows_per_rank
+    rp, ci, va, b, ys, m1l, (lo, up, xs, zs), cpart = generate_planted_block(
+        4, m1, m - m1, C4_N, C4_PER_ROW, r0, r1, cols)
+    if dist is not None:
+        t = torch.from_numpy(cpart).to(f"cuda:{local}")
+        dist.all_reduce(t)
+        cpart = t.cpu().numpy()
+    c = cpart + zs
+    return (rp, ci, va, m1l, b, c, lo, up), m, m1, r0
+
+
+def run_c4(args, dist, ws, rank, local):
+    import torch
+    import paper_2408_12179_b200 as P
+    from paper_2408_12179_b200.driver import LAMBDA_SAFETY
+    from paper_2408_12179_b200.rowblock import RowBlockGroup, broadcast_nccl_id, nccl_unique_id
+    rows = args.c4_rows
+    block, m, m1, r0 = c4_block(rank, ws, rows, local, dist)
+    nid = broadcast_nccl_id(rank) if dist is not None else nccl_unique_id()
+    grp = RowBlockGroup.distributed(block, n=C4_N, m_total=m, m1_total=m1,
+                                    nnz_total=m * C4_PER_ROW, row0=r0, rank=rank, world=ws,
+                                    nccl_id=nid, device=local)
+    grp.analyze()
+    grp.scale(10, True, True)
+    est = grp.power(1e-4, 5000)
+    lam = est.raw * (1.0 + LAMBDA_SAFETY)
+    grp.state_reset()
+    interval = 150
+    k = 0
+
+    def step():
+        nonlocal k
+        grp.run_inner(interval, k, k, 1.0, lam, 2)
+        grp.checkpoint(1.0, lam, 1, 0)
+        k += interval
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-        dist.destroy_process_group()
+    sample_clocks = ClockSampler(local)
+    inner_s = 0.0
+    l0 = grp.launch_count()
+    with sample_clocks:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(grp.stream)
+        for _ in range(args.steps):
+            step()
+            inner_s += grp.last_times()[0]
+        ev1.record(grp.stream)
+        ev1.synchronize()
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    launches = grp.launch_count() - l0
+    t_max, _ = _max_sum(dist, local, t_local, 0)
+    its = interval * args.steps
+    value = its / t_max               # every rank advances the same iterations
+    nnz_rank = rows * C4_PER_ROW
+    peak, peak_kind = load_peaks()
+    bi_rank = b_iter(rows, C4_N, nnz_rank)
+    achieved = bi_rank * its / inner_s / 1e9
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "hpr_iterations_per_sec", "value": value, "unit": "it/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES["c4"], "m": m, "n": C4_N,
+                       "nnz": m * C4_PER_ROW, "rows_per_rank": rows,
+                       "step": "150 HPR iterations + checkpoint (row-block, NCCL RS/AG per iteration)",
+                       "lambda": lam, "power_iterations": est.iterations,
+                       "l2": "working set > L2 (no flush needed)",
+                       "parallelism": f"row-block x{ws} (NCCL)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "per-rank iteration (A_g^T partial + slice x-phase + A_g y-phase + collectives)",
+                         "bytes_per_iteration": bi_rank, "peak_source": peak_kind},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": launches,
+            "clocks": sample_clocks.summary(),
+        }
+    grp.close()
+    _finish(dist, line, rank)
     return line
 
 
@@ -296,7 +580,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIG_NAMES), default="c2")
+    ap.add_argument("--c4-rows", type=int, default=1_250_000,
+                    help="rows per rank of the c4 weak-scaling instance (100 nnz each)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu DRAM bytes per iteration of the kernel pair (from profiles/)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

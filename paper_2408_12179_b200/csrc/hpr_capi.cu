@@ -44,6 +44,9 @@ int fail(int code, const std::string &msg) {
       return fail(HPR_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));     \
   } while (0)
 
+#ifndef HPR_WIDE_MIN
+#define HPR_WIDE_MIN 1000000  // avg row length from which a lane keeps 8 entries in flight (measured: U=8 loses, 124 regs)
+#endif
 constexpr int kPowBatch = 8;      // power steps per graph replay
 constexpr int kMaxGridPerSm = 8;  // CTAs per SM cap of the SELL kernels (partials sizing)
 constexpr int kSumsqBlocks = 1024;
@@ -174,8 +177,9 @@ struct hpr_ctx {
   long long launches = 0;
 
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
+    const int wide = S.nslices > 0 && S.slots >= (long long)HPR_WIDE_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
-                   S.long_rows, S.nslices, S.nlong};
+                   S.long_rows, S.nslices, S.nlong, wide};
   }
   SellMat mat_a(bool scaled) const {
     return mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
@@ -189,22 +193,30 @@ namespace {
 
 // Launch the SELL kernel for epilogue Epi: grid = min(windows, occupancy x SMs);
 // returns the grid (= partials per quantity).
-template <class Epi>
-int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
-                int *grid_out) {
+template <int U, class Epi>
+int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
+                  int *grid_out) {
   static int occ = 0;
   if (occ == 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<Epi>, kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, Epi>, kThreads, 0));
     if (occ < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
     occ = std::min(occ, kMaxGridPerSm);
   }
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
-  k_sell<Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
+  k_sell<U, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
   CKL();
   c->launches += 1;
   if (grid_out) *grid_out = grid;
   return HPR_OK;
+}
+
+// entries in flight per lane follow the matrix's average row length
+template <class Epi>
+int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
+                int *grid_out) {
+  return M.wide ? launch_sell_u<8>(c, M, xg, epi, part, grid_out)
+                : launch_sell_u<4>(c, M, xg, epi, part, grid_out);
 }
 
 // parts layout inside ctx->part (in doubles)

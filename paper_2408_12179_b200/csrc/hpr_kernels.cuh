@@ -75,6 +75,7 @@ struct SellMat {
   const int *long_rows;
   int nslices;
   int nlong;
+  int wide;                // average slice row length >= 6: 8 entries per lane in flight
 };
 
 constexpr int kSlice = 32;
@@ -148,47 +149,57 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 //   bool enter();                                 uniform early-out (power method)
 //   void prefetch(int r);                         load the row's operand vectors
 //   void finish(int r, double s, double *acc);    fused elementwise + reduction terms
-template <class Epi>
-__device__ __forceinline__ void sell_slice(const SellMat &M, int s, int lane,
+// per-lane slice header: the lane's row and length, the slice's slot range
+struct SliceHdr {
+  int row, len, base, slen;
+};
+__device__ __forceinline__ SliceHdr load_hdr(const SellMat &M, int s, int lane) {
+  SliceHdr h{-1, 0, 0, 0};
+  if (s < M.nslices) {
+    h.row = M.slice_row[s * kSlice + lane];
+    h.len = M.slice_len[s * kSlice + lane];
+    h.base = M.slice_ptr[s];
+    h.slen = (M.slice_ptr[s + 1] - h.base) / kSlice;
+  }
+  return h;
+}
+
+template <int U, class Epi>
+__device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
-  // row, length and the slice's slot range are independent loads (no chain
-  // through the CSR row pointers)
-  const int row = M.slice_row[s * kSlice + lane];
-  const int len = M.slice_len[s * kSlice + lane];
-  const int base = M.slice_ptr[s];
-  const int slen = (M.slice_ptr[s + 1] - base) / kSlice;
+  const int row = h.row, len = h.len, slen = h.slen;
   if (row >= 0) epi.prefetch(row);
-  const int *cp = M.ci + base + lane;
-  const double *vp = M.val + base + lane;
+  const int *cp = M.ci + h.base + lane;
+  const double *vp = M.val + h.base + lane;
   double sum = 0.0;
   // software pipeline: the streaming loads of batch i+1 are in flight while
   // batch i's operand gathers complete and its products are added in order
-  int c[kUnroll];
-  double v[kUnroll];
+  int c[U];
+  double v[U];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u)
+  for (int u = 0; u < U; ++u)
     if (u < len) {
       c[u] = ld_stream(cp + u * kSlice, pol);
       v[u] = ld_stream(vp + u * kSlice, pol);
     }
-  for (int k = 0; k < slen; k += kUnroll) {
-    int cn[kUnroll];
-    double vn[kUnroll], xv[kUnroll];
+  for (int k = 0; k < slen; k += U) {
+    int cn[U];
+    double vn[U], xv[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (k + kUnroll + u < len) {
-        cn[u] = ld_stream(cp + (k + kUnroll + u) * kSlice, pol);
-        vn[u] = ld_stream(vp + (k + kUnroll + u) * kSlice, pol);
+    for (int u = 0; u < U; ++u)
+      if (k + U + u < len) {
+        cn[u] = ld_stream(cp + (k + U + u) * kSlice, pol);
+        vn[u] = ld_stream(vp + (k + U + u) * kSlice, pol);
       }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+    for (int u = 0; u < U; ++u)
       if (k + u < len) xv[u] = __ldg(xg + c[u]);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+    for (int u = 0; u < U; ++u)
       if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       c[u] = cn[u];
       v[u] = vn[u];
     }
@@ -265,7 +276,7 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
 // One CTA = 8 warps; CTA c handles sorting windows c, c + G, ... (warp w takes
 // slice 8*window + w), then the long rows are strided over all warps.  Static
 // assignment keeps the per-CTA partial sums deterministic.
-template <class Epi>
+template <int U, class Epi>
 __global__ void __launch_bounds__(kThreads)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
@@ -275,9 +286,13 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  // the next window's slice header is loaded while this one is processed, so
+  // a slice costs two dependent memory round trips (matrix, gather), not three
+  SliceHdr h = load_hdr(M, blockIdx.x * kWarpsPerCta + wib, lane);
   for (int win = blockIdx.x; win < nwin; win += gridDim.x) {
-    const int sl = win * kWarpsPerCta + wib;
-    if (sl < M.nslices) sell_slice(M, sl, lane, xg, epi, acc, pol);
+    const SliceHdr hn = load_hdr(M, (win + gridDim.x) * kWarpsPerCta + wib, lane);
+    sell_slice<U>(M, h, lane, xg, epi, acc, pol);
+    h = hn;
   }
   for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += gridDim.x * kWarpsPerCta)
     long_row(M, M.long_rows[li], lane, xg, epi, acc, pol);

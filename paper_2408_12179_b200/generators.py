@@ -275,6 +275,96 @@ def generate_planted_lp_fast(seed: int, m1: int, m2: int, n: int, per_row: int):
     return prob, PrimalDualPoint(y=y, z=z, x=x)
 
 
+# ---------------------------------------------------------------------------
+# C4: one rank's row block of a planted LP, generated independently per rank
+# ---------------------------------------------------------------------------
+
+_CHUNK = 1 << 16
+
+
+def _planted_columns(seed, n):
+    """Bounds, x*, z* of the planted LP (identical on every rank)."""
+    rng = np.random.default_rng([seed, 0])
+    lower = np.zeros(n)
+    upper = np.full(n, np.inf)
+    kinds = rng.choice(4, size=n, p=[0.6, 0.2, 0.1, 0.1])
+    boxed = kinds == 1
+    lower[boxed] = rng.uniform(-1.0, 0.5, size=int(boxed.sum()))
+    upper[boxed] = lower[boxed] + rng.uniform(0.5, 2.0, size=int(boxed.sum()))
+    lower[kinds >= 2] = -np.inf
+    upper[kinds == 3] = rng.uniform(0.0, 2.0, size=int((kinds == 3).sum()))
+    roll = rng.uniform(size=n)
+    x = np.empty(n)
+    z = np.zeros(n)
+    at_lo = (roll < 0.2) & np.isfinite(lower)
+    at_up = ~at_lo & (roll < 0.4) & np.isfinite(upper)
+    inter = ~(at_lo | at_up)
+    x[at_lo] = lower[at_lo]
+    z[at_lo] = rng.uniform(0.3, 1.5, size=int(at_lo.sum()))
+    x[at_up] = upper[at_up]
+    z[at_up] = -rng.uniform(0.3, 1.5, size=int(at_up.sum()))
+    a0 = np.where(np.isfinite(lower), lower, -1.5)
+    b0 = np.where(np.isfinite(upper), upper, a0 + 3.0)
+    wide = inter & (b0 - a0 > 0.2)
+    x[wide] = rng.uniform(a0[wide] + 0.1, b0[wide] - 0.1)
+    narrow = inter & ~wide
+    x[narrow] = lower[narrow]
+    z[narrow] = rng.uniform(0.3, 1.5, size=int(narrow.sum()))
+    return lower, upper, x, z
+
+
+def generate_planted_block(seed: int, m1: int, m2: int, n: int, per_row: int, r0: int, r1: int,
+                           columns=None):
+    """Rows [r0, r1) of the C4 planted LP (distribution of mps.py:524-610).
+
+    Rows are drawn in chunks of 65536 from ``default_rng([seed, 1 + chunk])``,
+    so a row's content does not depend on how the rows are split over ranks.
+    Returns ``(row_offsets, col_indices, values, b_block, y_block, m1_local,
+    (lower, upper, x*, z*), c_partial)`` where ``c_partial = A_block^T y*_block``
+    -- summing it over all blocks and adding z* gives the cost vector.
+    """
+    lower, upper, xs, zs = columns if columns is not None else _planted_columns(seed, n)
+    rows = r1 - r0
+    cols = np.empty((rows, per_row), dtype=np.int64)
+    vals = np.empty((rows, per_row))
+    ys = np.empty(rows)
+    slack = np.zeros(rows)
+    for ch in range(r0 // _CHUNK, (r1 - 1) // _CHUNK + 1):
+        c0, c1 = ch * _CHUNK, min((ch + 1) * _CHUNK, m1 + m2)
+        rng = np.random.default_rng([seed, 1 + ch])
+        cc = np.sort(rng.integers(0, n, size=(c1 - c0, per_row), dtype=np.int64), axis=1)
+        for _ in range(64):
+            dup = np.zeros_like(cc, dtype=bool)
+            dup[:, 1:] = cc[:, 1:] == cc[:, :-1]
+            nd = int(dup.sum())
+            if nd == 0:
+                break
+            cc[dup] = rng.integers(0, n, size=nd, dtype=np.int64)
+            cc.sort(axis=1)
+        vv = rng.uniform(-2.0, 2.0, size=(c1 - c0, per_row))
+        tiny = np.abs(vv) < 0.1
+        vv[tiny] += np.sign(vv[tiny] + 0.5) * 0.5
+        gi = np.arange(c0, c1)
+        yy = rng.normal(size=c1 - c0)
+        active = rng.uniform(size=c1 - c0) < 0.5
+        ineq = gi >= m1
+        yy[ineq] = np.where(active[ineq], rng.uniform(0.3, 1.5, size=int(ineq.sum())), 0.0)
+        sl = np.where(ineq & ~active, rng.uniform(0.5, 2.0, size=c1 - c0), 0.0)
+        lo, hi = max(c0, r0), min(c1, r1)
+        cols[lo - r0:hi - r0] = cc[lo - c0:hi - c0]
+        vals[lo - r0:hi - r0] = vv[lo - c0:hi - c0]
+        ys[lo - r0:hi - r0] = yy[lo - c0:hi - c0]
+        slack[lo - r0:hi - r0] = sl[lo - c0:hi - c0]
+    rp = np.arange(0, rows * per_row + 1, per_row, dtype=np.int64)
+    ci = cols.reshape(-1)
+    va = vals.reshape(-1)
+    a = sp.csr_matrix((va, ci, rp), shape=(rows, n))
+    b = a @ xs - slack
+    c_partial = a.T @ ys
+    m1_local = int(min(max(m1 - r0, 0), rows))
+    return rp, ci, va, b, ys, m1_local, (lower, upper, xs, zs), c_partial
+
+
 # named benchmark configurations (SURVEY.md §8(d))
 def config_instance(name: str):
     name = name.lower()

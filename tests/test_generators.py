@@ -82,3 +82,29 @@ def test_planted_fast_generator_is_kkt():
     assert np.all(a[p.m1:] @ pt.x - p.b_ineq >= -1e-12)
     assert np.max(np.abs(a.T @ pt.y + pt.z - p.c)) <= 1e-12
     assert np.all((pt.x >= p.lower) & (pt.x <= p.upper))
+
+
+def test_planted_block_generator_split_invariant_and_kkt():
+    """C4 row blocks: identical rows under any split; the assembled problem has
+    the planted point as an exact KKT point (oracle kkt_residual)."""
+    from oracle import hprlp_oracle as O
+    from paper_2408_12179_b200 import LpProblem, SparseMatrix
+    from paper_2408_12179_b200.generators import _planted_columns, generate_planted_block
+    m1, m2, n, per = 300, 400, 3000, 12
+    cols = _planted_columns(4, n)
+    whole = generate_planted_block(4, m1, m2, n, per, 0, m1 + m2, cols)
+    parts = [generate_planted_block(4, m1, m2, n, per, a, b, cols)
+             for a, b in ((0, 123), (123, 500), (500, 700))]
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), whole[1])
+    assert np.array_equal(np.concatenate([p[2] for p in parts]), whole[2])
+    assert np.array_equal(np.concatenate([p[3] for p in parts]), whole[3])
+    assert [p[5] for p in parts] == [123, 177, 0]
+    rp, ci, va, b, ys, _, (lo, up, xs, zs), cpart = whole
+    c = cpart + zs
+    prob = LpProblem(a_eq=SparseMatrix.from_csr_arrays(rp[:m1 + 1], ci[:rp[m1]], va[:rp[m1]], m1, n),
+                     a_ineq=SparseMatrix.from_csr_arrays(rp[m1:] - rp[m1], ci[rp[m1]:], va[rp[m1]:],
+                                                         m2, n),
+                     b_eq=b[:m1], b_ineq=b[m1:], c=c, lower=lo, upper=up)
+    res = O.kkt(O.OracleLP.from_problem(prob), ys, zs, xs)
+    assert res["primal_infeas_rel"] < 1e-12 and res["dual_infeas_rel"] < 1e-12
+    assert res["gap_rel"] < 1e-11
