@@ -276,8 +276,11 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
 // One CTA = 8 warps; CTA c handles sorting windows c, c + G, ... (warp w takes
 // slice 8*window + w), then the long rows are strided over all warps.  Static
 // assignment keeps the per-CTA partial sums deterministic.
+#ifndef HPR_SELL_MINB
+#define HPR_SELL_MINB 1      // min resident CTAs per SM requested from ptxas (register cap)
+#endif
 template <int U, class Epi>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, HPR_SELL_MINB)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll

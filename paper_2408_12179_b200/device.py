@@ -19,11 +19,11 @@ again for the unscaled values (KKT residuals use the user's matrix).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
 from . import _native as N
-from .problem import stacked_arrays
 
 PAD = 8   # trailing slots on every nonzero array (16-byte bulk-copy rounding)
 
@@ -33,15 +33,39 @@ def _torch():
     return torch
 
 
+class _Staging:
+    """Process-wide pinned host staging buffer for uploads (grown on demand,
+    reused across problems: no per-upload page-locking)."""
+
+    buf = None
+    lock = threading.Lock()
+
+    @classmethod
+    def get(cls, nbytes):
+        torch = _torch()
+        if cls.buf is None or cls.buf.numel() < nbytes:
+            cls.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        return cls.buf
+
+
+def _csr_parts(problem):
+    """The stacked A = [A_eq; A_ineq] as (row_offsets, col_indices, values)
+    pieces, written straight into the staging buffer (problem.py:75-82)."""
+    top, bot = problem.a_eq, problem.a_ineq
+    return [(np.asarray(top.row_offsets), np.asarray(top.col_indices), np.asarray(top.values)),
+            (np.asarray(bot.row_offsets), np.asarray(bot.col_indices), np.asarray(bot.values))]
+
+
 class DeviceLP:
     """Uploads a reference-shaped LpProblem and owns its native context."""
 
     def __init__(self, problem, device: int = 0, stream=None, pinned_upload: bool = True):
-        ro, ci, v, m, n, m1 = stacked_arrays(problem)
-        rhs = np.concatenate([np.asarray(problem.b_eq, np.float64),
-                              np.asarray(problem.b_ineq, np.float64)])
-        self._setup(ro, ci, v, m, n, m1, rhs, problem.c, problem.lower, problem.upper,
-                    device=device, stream=stream, pinned_upload=pinned_upload)
+        parts = _csr_parts(problem)
+        m1 = int(problem.a_eq.nrows)
+        m = m1 + int(problem.a_ineq.nrows)
+        n = int(problem.a_eq.ncols)
+        self._setup(parts, m, n, m1, (problem.b_eq, problem.b_ineq), problem.c, problem.lower,
+                    problem.upper, device=device, stream=stream)
 
     @classmethod
     def from_arrays(cls, ro, ci, v, m, n, m1, b, c, lower, upper, *, device: int = 0,
@@ -49,17 +73,17 @@ class DeviceLP:
         """A row block [rows of A, all n columns] (row-block mode): column vectors
         are allocated at ``n_alloc >= n`` (the group's padded length)."""
         self = cls.__new__(cls)
-        self._setup(ro, ci, v, m, n, m1, b, c, lower, upper, device=device, stream=stream,
-                    pinned_upload=pinned_upload, n_alloc=n_alloc)
+        self._setup([(np.asarray(ro), np.asarray(ci), np.asarray(v))], m, n, m1, (b,), c, lower,
+                    upper, device=device, stream=stream, n_alloc=n_alloc)
         return self
 
-    def _setup(self, ro, ci, v, m, n, m1, rhs, c, lower, upper, *, device, stream,
-               pinned_upload, n_alloc=None):
+    def _setup(self, parts, m, n, m1, rhs_parts, c, lower, upper, *, device, stream,
+               n_alloc=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise N.NativeUnavailableError("CUDA device required: the HPR-LP path has no CPU fallback")
         N.load_library()
-        nnz = int(ro[-1])
+        nnz = int(sum(int(ro[-1]) - int(ro[0]) for ro, _, _ in parts))
         if nnz >= 2**31 - 1 or m >= 2**31 - 1 or n >= 2**31 - 1:
             raise ValueError("problem exceeds int32 indexing of this build")
         self.m, self.n, self.m1, self.nnz = m, n, m1, nnz
@@ -67,31 +91,66 @@ class DeviceLP:
         self.n_alloc = na
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
-        self.h2d_bytes = 0
         dev = self.device
         f64 = dict(dtype=torch.float64, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
-        with torch.cuda.stream(self.stream):
-            def up(arr, dtype, length=None):
-                a = np.ascontiguousarray(arr, dtype=dtype)
-                if length is not None and length > a.size:
-                    a = np.concatenate([a, np.zeros(length - a.size, dtype=dtype)])
-                t = torch.from_numpy(a)
-                if pinned_upload:
-                    t = t.pin_memory()
-                self.h2d_bytes += t.numel() * t.element_size()
-                return t.to(dev, non_blocking=True)
+        nz1 = nnz + PAD
 
-            T = {}
-            # nonzero arrays carry PAD trailing slots: the tile engine's bulk copies
-            # round every tile up to 16-byte boundaries
-            T["a_rp"] = up(ro, np.int32)
-            T["a_ci"] = up(np.concatenate([ci, np.zeros(PAD)]), np.int32)
-            T["a_val"] = up(np.concatenate([v, np.zeros(PAD)]), np.float64)
-            T["b"] = up(rhs, np.float64)
-            T["c"] = up(c, np.float64, na)
-            T["lower"] = up(lower, np.float64, na)
-            T["upper"] = up(upper, np.float64, na)
+        # host inputs -> one pinned staging buffer -> one H2D copy; every input
+        # array is a view of the device copy.  Writers cast in place (int64 ->
+        # int32), so no host temporaries are made.
+        def w_rp(dst):
+            off, r = 0, 0
+            for ro, _, _ in parts:
+                k = len(ro) - 1
+                np.copyto(dst[r:r + k], ro[:-1] - ro[0] + off, casting="unsafe")
+                off += int(ro[-1]) - int(ro[0])
+                r += k
+            dst[r] = off
+
+        def w_nz(which, pad):
+            def fill(dst):
+                o = 0
+                for piece in parts:
+                    a = piece[which]
+                    np.copyto(dst[o:o + a.size], a, casting="unsafe")
+                    o += a.size
+                dst[o:] = pad
+            return fill
+
+        def w_vec(arrs, length):
+            def fill(dst):
+                o = 0
+                for a in arrs:
+                    a = np.asarray(a)
+                    np.copyto(dst[o:o + a.size], a, casting="unsafe")
+                    o += a.size
+                dst[o:length] = 0.0
+            return fill
+
+        spec = [("a_rp", np.int32, m + 1, w_rp), ("a_ci", np.int32, nz1, w_nz(1, 0)),
+                ("a_val", np.float64, nz1, w_nz(2, 0.0)), ("b", np.float64, m, w_vec(rhs_parts, m)),
+                ("c", np.float64, na, w_vec((c,), na)), ("lower", np.float64, na, w_vec((lower,), na)),
+                ("upper", np.float64, na, w_vec((upper,), na))]
+        offs, total = [], 0
+        for _, dt, ln, _ in spec:
+            offs.append(total)
+            total += (ln * np.dtype(dt).itemsize + 255) // 256 * 256
+        T = {}
+        with _Staging.lock:
+            stage = _Staging.get(total)
+            host = stage.numpy()
+            for (name, dt, ln, fill), o in zip(spec, offs):
+                fill(host[o:o + ln * np.dtype(dt).itemsize].view(dt))
+            with torch.cuda.stream(self.stream):
+                self._inputs = torch.empty(total, dtype=torch.uint8, device=dev)
+                self._inputs.copy_(stage[:total], non_blocking=True)
+            self.stream.synchronize()       # the staging buffer is reusable after this
+        tdt = {np.int32: torch.int32, np.float64: torch.float64}
+        for (name, dt, ln, _), o in zip(spec, offs):
+            T[name] = self._inputs[o:o + ln * np.dtype(dt).itemsize].view(tdt[dt])
+        self.h2d_bytes = total
+        with torch.cuda.stream(self.stream):
             nz1 = nnz + PAD
             T["a_val_s"] = torch.empty(nz1, **f64)
             T["at_rp"] = torch.empty(n + 1, **i32)
