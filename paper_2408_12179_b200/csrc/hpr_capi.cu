@@ -18,6 +18,7 @@
 
 #include "../../include/hprlp_b200.h"
 #include "hpr_kernels.cuh"
+#include "hpr_cb.cuh"
 
 using namespace hpr;
 
@@ -67,8 +68,38 @@ struct PlanOff {
   size_t slice_row, slice_len, slice_slots, slice_ptr, long_flag, long_rows, nsel;
 };
 
+// column-blocked (CB) engine plan arrays of one matrix (persistent, workspace)
+struct CbOff {
+  bool on = false;
+  int G = 0, NB = 0;
+  size_t row_start = 0, gstart = 0, gseg = 0, rpb_base = 0;
+};
+
+constexpr int kCbW = 8192;           // doubles per CB column block (64 KB)
+constexpr int kCbMaxSmem = 227 * 1024 - 1024;
+
+// The CB engine replaces L1TEX-bound random gathers by staging the operand
+// vector through shared memory; it pays a full pass over the vector per SM.
+// Model (B200): staging ~95 GB/s per SM, gathers ~0.55 x one L1TEX wavefront
+// per cycle.  Override with HPR_CB=0 (never) / HPR_CB=1 (whenever it fits).
+bool cb_wanted(int64_t rows, int64_t cols, int64_t nnz) {
+  if (rows < 1 || cols < 1 || nnz < 1) return false;
+  const int64_t NB = (cols + kCbW - 1) / kCbW;
+  if (NB > 4096) return false;
+  const char *env = getenv("HPR_CB");
+  if (env && env[0] == '0') return false;
+  if (env && env[0] == '1') return true;
+  if (!(env && env[0] == 'a')) return false;   // measured slower than SELL on C2 so far: opt-in
+  const double G = 148.0;
+  const double t_cb = cols * 8.0 / 95e9 + (10.0 * nnz + 4.0 * rows * NB) / (G * 95e9);
+  const double t_sell = nnz / (G * 1.92e9 * 0.55);
+  return t_cb < 0.8 * t_sell;
+}
+
 struct Layout {
   PlanOff pa, pat;
+  CbOff ca, cat;
+  size_t cb_key = 0, cb_lrow = 0;
   size_t keys_out, iota, row_of, cub_tmp, cub_bytes, dvec_m, dvec_n, part, part_count, params,
       pow, results, fac, flags, total;
 };
@@ -110,6 +141,25 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
   };
   L.pa = plan(d.m);
   L.pat = plan(d.n);
+  auto cbplan = [&](int64_t rows, int64_t cols) {
+    CbOff o;
+    o.on = cb_wanted(rows, cols, d.nnz);
+    if (!o.on) return o;
+    o.G = (int)std::min<int64_t>(148 * 8, rows);     // placeholder upper bound, fixed at analyze
+    o.NB = (int)((cols + kCbW - 1) / kCbW);
+    const int64_t ng = (int64_t)o.G * o.NB;
+    o.row_start = take(sizeof(int) * (o.G + 1));
+    o.gstart = take(sizeof(int) * (ng + 1));
+    o.gseg = take(sizeof(long long) * (ng + 1));
+    o.rpb_base = take(sizeof(long long) * (ng + 1));
+    return o;
+  };
+  L.ca = cbplan(d.m, d.n);
+  L.cat = cbplan(d.n, d.m);
+  if (L.ca.on || L.cat.on) {
+    L.cb_key = take(sizeof(int) * d.nnz);
+    L.cb_lrow = take(sizeof(int) * d.nnz);
+  }
   L.keys_out = take(sizeof(int) * d.nnz);
   L.iota = take(sizeof(int) * d.nnz);
   L.row_of = take(sizeof(int) * d.nnz);
@@ -160,6 +210,15 @@ struct hpr_ctx {
   char *ws = nullptr;
   Layout L{};
   Sell sa, sat;
+  struct Cb {
+    bool on = false;
+    int G = 0, NB = 0, rows_cap = 0, seg_cap = 0, smem = 0;
+    long long npad = 0, nrpb = 0;
+    int *row_start = nullptr, *gstart = nullptr, *rpb = nullptr;
+    long long *gseg = nullptr, *rpb_base = nullptr, *pos = nullptr;
+    unsigned short *ci = nullptr;
+    double *val = nullptr;
+  } cba, cbat;
   int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
@@ -180,6 +239,10 @@ struct hpr_ctx {
     const int wide = S.nslices > 0 && S.slots >= (long long)HPR_WIDE_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
                    S.long_rows, S.nslices, S.nlong, wide};
+  }
+  CbMat cbmat(const Cb &C, int ncols) const {
+    return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
+                 C.rows_cap, C.seg_cap};
   }
   SellMat mat_a(bool scaled) const {
     return mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
@@ -301,6 +364,112 @@ int layout_sell(hpr_ctx *c, char *&p, Sell &S, const int *rp, const int *ci, con
     CKL();
   }
   c->launches += 2;
+  return HPR_OK;
+}
+
+// ---- CB engine: plan (hpr_analyze) and layout (hpr_bind_layout) ----
+// keys + stable sort of the entries by (CTA, column block); leaves the sorted
+// keys in L.keys_out, the permutation in L.row_of, local rows in L.cb_lrow
+int cb_sort(hpr_ctx *c, const hpr_ctx::Cb &C, const int *rp, const int *ci) {
+  cudaStream_t s = c->stream;
+  const long long nnz = c->d.nnz;
+  int *key = (int *)(c->ws + c->L.cb_key), *lrow = (int *)(c->ws + c->L.cb_lrow);
+  int *skey = (int *)(c->ws + c->L.keys_out), *iota = (int *)(c->ws + c->L.iota);
+  int *perm = (int *)(c->ws + c->L.row_of);
+  k_cb_keys<<<C.G, 256, 0, s>>>(rp, ci, C.row_start, C.G, C.NB, kCbW, key, lrow);
+  k_iota<<<grid_for(nnz), 256, 0, s>>>(iota, nnz);
+  CKL();
+  int end_bit = 1;
+  while ((1LL << end_bit) < (long long)C.G * C.NB) ++end_bit;
+  size_t tb = c->L.cub_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(c->ws + c->L.cub_tmp, tb, key, skey, iota, perm, (int)nnz, 0,
+                                     end_bit, s));
+  c->launches += 4;
+  return HPR_OK;
+}
+
+int cb_plan(hpr_ctx *c, const CbOff &o, const int *rp, const int *ci, int rows, hpr_ctx::Cb &C) {
+  C = hpr_ctx::Cb{};
+  if (!o.on || c->d.nnz == 0) return HPR_OK;
+  cudaStream_t s = c->stream;
+  C.G = std::min(c->num_sms, rows);
+  if (C.G > std::min<int64_t>(148 * 8, rows)) return HPR_OK;     // workspace sized for fewer
+  C.NB = o.NB;
+  C.row_start = (int *)(c->ws + o.row_start);
+  C.gstart = (int *)(c->ws + o.gstart);
+  C.gseg = (long long *)(c->ws + o.gseg);
+  C.rpb_base = (long long *)(c->ws + o.rpb_base);
+  k_cb_rowstart<<<1, 1, 0, s>>>(rp, rows, C.G, C.row_start);
+  CKL();
+  int rc = cb_sort(c, C, rp, ci);
+  if (rc) return rc;
+  const long long ng = (long long)C.G * C.NB;
+  k_cb_count<<<grid_for(c->d.nnz), 256, 0, s>>>((int *)(c->ws + c->L.keys_out), c->d.nnz, (int)ng,
+                                                C.gstart);
+  k_cb_pad<<<1, 1, 0, s>>>(C.gstart, C.row_start, C.G, C.NB, C.gseg, C.rpb_base);
+  CKL();
+  c->launches += 3;
+  std::vector<int> hrs(C.G + 1);
+  std::vector<long long> hseg(ng + 1);
+  CK(cudaMemcpyAsync(hrs.data(), C.row_start, sizeof(int) * (C.G + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hseg.data(), C.gseg, sizeof(long long) * (ng + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int g = 0; g < C.G; ++g) {
+    const int rg = hrs[g + 1] - hrs[g];
+    C.rows_cap = std::max(C.rows_cap, rg);
+    C.nrpb += (long long)C.NB * ((rg + 1 + 3) / 4 * 4);
+  }
+  for (long long q = 0; q < ng; ++q) C.seg_cap = (int)std::max<long long>(C.seg_cap, hseg[q + 1] - hseg[q]);
+  C.npad = hseg[ng];
+  C.smem = cb_smem(kCbW, C.seg_cap, C.rows_cap).total;
+  C.on = C.smem <= kCbMaxSmem && C.npad < INT_MAX;
+  return HPR_OK;
+}
+
+size_t cb_bytes(const hpr_ctx::Cb &C, int64_t nnz) {
+  if (!C.on) return 0;
+  return align_up((size_t)C.npad * 8 + 256, 256) + align_up((size_t)C.npad * 2 + 256, 256) +
+         align_up((size_t)C.nrpb * 4 + 256, 256) + align_up((size_t)nnz * 8 + 256, 256);
+}
+
+int cb_layout(hpr_ctx *c, char *&p, hpr_ctx::Cb &C, const int *rp, const int *ci) {
+  if (!C.on) return HPR_OK;
+  cudaStream_t s = c->stream;
+  const long long nnz = c->d.nnz;
+  C.val = (double *)p;
+  p += align_up((size_t)C.npad * 8 + 256, 256);
+  C.ci = (unsigned short *)p;
+  p += align_up((size_t)C.npad * 2 + 256, 256);
+  C.rpb = (int *)p;
+  p += align_up((size_t)C.nrpb * 4 + 256, 256);
+  C.pos = (long long *)p;
+  p += align_up((size_t)nnz * 8 + 256, 256);
+  CK(cudaMemsetAsync(C.val, 0, (size_t)C.npad * 8, s));
+  CK(cudaMemsetAsync(C.ci, 0, (size_t)C.npad * 2, s));
+  CK(cudaMemsetAsync(C.rpb, 0, (size_t)C.nrpb * 4, s));
+  int rc = cb_sort(c, C, rp, ci);
+  if (rc) return rc;
+  const long long ng = (long long)C.G * C.NB;
+  k_cb_empty<<<(int)ng, 128, 0, s>>>(C.gstart, C.rpb_base, C.row_start, C.G, C.NB, C.rpb);
+  k_cb_fill<<<grid_for(nnz), 256, 0, s>>>((int *)(c->ws + c->L.keys_out), (int *)(c->ws + c->L.row_of),
+                                          (int *)(c->ws + c->L.cb_lrow), ci, C.gstart, C.gseg,
+                                          C.rpb_base, C.row_start, C.NB, kCbW, nnz, C.ci, C.rpb,
+                                          C.pos);
+  CKL();
+  c->launches += 2;
+  return HPR_OK;
+}
+
+template <class Epi>
+int launch_cb(hpr_ctx *c, const hpr_ctx::Cb &C, int ncols, const double *xg, const Epi &epi) {
+  static int smem_set = 0;
+  if (C.smem > smem_set) {
+    CK(cudaFuncSetAttribute(k_cb<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
+    smem_set = kCbMaxSmem;
+  }
+  k_cb<Epi><<<C.G, kCbThreads, C.smem, c->stream>>>(c->cbmat(C, ncols), xg, epi, nullptr);
+  CKL();
+  c->launches += 1;
   return HPR_OK;
 }
 
@@ -535,7 +704,12 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   if (rc) return rc;
   rc = plan_sell(c, c->L.pat, B.at_rp, n, c->sat);
   if (rc) return rc;
-  *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz);
+  rc = cb_plan(c, c->L.ca, B.a_rp, B.a_ci, m, c->cba);
+  if (rc) return rc;
+  rc = cb_plan(c, c->L.cat, B.at_rp, B.at_ci, n, c->cbat);
+  if (rc) return rc;
+  *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz) +
+                  cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz);
   c->analyzed = true;
   c->laid_out = false;
   return HPR_OK;
@@ -546,7 +720,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (rc) return rc;
   if (!c->analyzed) return fail(HPR_ESTATE, "hpr_analyze has not been called");
   if (!layout) return fail(HPR_EINVAL, "null layout");
-  if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz))
+  if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz) +
+                  cb_bytes(c->cba, c->d.nnz) + cb_bytes(c->cbat, c->d.nnz))
     return fail(HPR_EINVAL, "layout buffer too small");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
@@ -554,6 +729,10 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   rc = layout_sell(c, p, c->sa, B.a_rp, B.a_ci, B.a_val);
   if (rc) return rc;
   rc = layout_sell(c, p, c->sat, B.at_rp, B.at_ci, B.at_val);
+  if (rc) return rc;
+  rc = cb_layout(c, p, c->cba, B.a_rp, B.a_ci);
+  if (rc) return rc;
+  rc = cb_layout(c, p, c->cbat, B.at_rp, B.at_ci);
   if (rc) return rc;
   CK(cudaStreamSynchronize(c->stream));
   for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
@@ -631,6 +810,10 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
     k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sat.pos, B.at_val_s, c->sat.val_s, nnz);
     CKL();
     c->launches += 3;
+    if (c->cba.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cba.pos, B.a_val_s, c->cba.val, nnz);
+    if (c->cbat.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cbat.pos, B.at_val_s, c->cbat.val, nnz);
+    CKL();
+    c->launches += (int)c->cba.on + (int)c->cbat.on;
   }
   // ||b||, ||c|| of the original and the scaled problem (relative residual denominators)
   const int nbm = sumsq_blocks(m), nbn = sumsq_blocks(n);
@@ -831,8 +1014,11 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     for (int i = 0; i < steps; ++i) {
       ex.step = i;
       ey.step = i;
-      int rc2 = launch_sell(c, AT, B.y, ex, nullptr, nullptr);
-      if (!rc2) rc2 = launch_sell(c, A, B.w, ey, nullptr, nullptr);
+      int rc2 = c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
+                           : launch_sell(c, AT, B.y, ex, nullptr, nullptr);
+      if (!rc2)
+        rc2 = c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
+                        : launch_sell(c, A, B.w, ey, nullptr, nullptr);
       if (rc2) {
         cudaStreamEndCapture(s, &g);
         return rc2;
@@ -991,6 +1177,8 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->slots_at = c->sat.slots;
   info->long_rows_a = c->sa.nlong;
   info->long_rows_at = c->sat.nlong;
+  info->cb_a = c->cba.on ? c->cba.npad : 0;
+  info->cb_at = c->cbat.on ? c->cbat.npad : 0;
   return HPR_OK;
 }
 

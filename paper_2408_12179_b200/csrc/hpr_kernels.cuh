@@ -75,7 +75,7 @@ struct SellMat {
   const int *long_rows;
   int nslices;
   int nlong;
-  int wide;                // average slice row length >= 6: 8 entries per lane in flight
+  int wide;                // long rows: 8 entries per lane in flight (HPR_WIDE_MIN)
 };
 
 constexpr int kSlice = 32;
@@ -84,6 +84,9 @@ constexpr int kLongRow = 1024;
 constexpr int kWarpsPerCta = kThreads / 32;
 #ifndef HPR_UNROLL
 #define HPR_UNROLL 4
+#endif
+#ifndef HPR_GATHER_AHEAD
+#define HPR_GATHER_AHEAD 0
 #endif
 constexpr int kUnroll = HPR_UNROLL;     // entries per lane in flight (x2: software pipelined)
 
@@ -183,6 +186,48 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       c[u] = ld_stream(cp + u * kSlice, pol);
       v[u] = ld_stream(vp + u * kSlice, pol);
     }
+#if HPR_GATHER_AHEAD
+  // depth-2 pipeline: batch k+1's operand gathers and batch k+2's matrix loads
+  // are in flight while batch k's products are added (long rows: the gather
+  // latency is exposed once per two batches instead of once per batch)
+  double x0[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < len) x0[u] = __ldg(xg + c[u]);
+  int c1[U];
+  double v1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (U + u < len) {
+      c1[u] = ld_stream(cp + (U + u) * kSlice, pol);
+      v1[u] = ld_stream(vp + (U + u) * kSlice, pol);
+    }
+  for (int k = 0; k < slen; k += U) {
+    double x1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + U + u < len) x1[u] = __ldg(xg + c1[u]);
+    int c2[U];
+    double v2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + 2 * U + u < len) {
+        c2[u] = ld_stream(cp + (k + 2 * U + u) * kSlice, pol);
+        v2[u] = ld_stream(vp + (k + 2 * U + u) * kSlice, pol);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], x0[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = v1[u];
+      x0[u] = x1[u];
+      c1[u] = c2[u];
+      v1[u] = v2[u];
+    }
+  }
+  if (false)
+#endif
   for (int k = 0; k < slen; k += U) {
     int cn[U];
     double vn[U], xv[U];
@@ -289,13 +334,16 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int G = gridDim.x;
   // the next window's slice header is loaded while this one is processed, so
   // a slice costs two dependent memory round trips (matrix, gather), not three
-  SliceHdr h = load_hdr(M, blockIdx.x * kWarpsPerCta + wib, lane);
-  for (int win = blockIdx.x; win < nwin; win += gridDim.x) {
-    const SliceHdr hn = load_hdr(M, (win + gridDim.x) * kWarpsPerCta + wib, lane);
-    sell_slice<U>(M, h, lane, xg, epi, acc, pol);
-    h = hn;
+  {
+    SliceHdr h = load_hdr(M, blockIdx.x * kWarpsPerCta + wib, lane);
+    for (int win = blockIdx.x; win < nwin; win += G) {
+      const SliceHdr hn = load_hdr(M, (win + G) * kWarpsPerCta + wib, lane);
+      sell_slice<U>(M, h, lane, xg, epi, acc, pol);
+      h = hn;
+    }
   }
   for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += gridDim.x * kWarpsPerCta)
     long_row(M, M.long_rows[li], lane, xg, epi, acc, pol);

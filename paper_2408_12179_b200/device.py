@@ -159,10 +159,11 @@ class DeviceLP:
             T["at_val"] = torch.empty(nz1, **f64)
             T["at_val_s"] = torch.empty(nz1, **f64)
             for name in ("b_s", "row_scale", "y", "anc_y", "yb", "dy"):
-                T[name] = torch.empty(m, **f64)
+                # gathered vectors are read in 16-byte bulk copies: keep slack after them
+                T[name] = torch.empty(m + 8, **f64)[:m]
             for name in ("c_s", "lower_s", "upper_s", "col_scale", "x", "anc_x", "w", "xb",
                          "zb", "wtmp"):
-                T[name] = torch.empty(na, **f64)
+                T[name] = torch.empty(na + 8, **f64)[:na]
             T["cand_y"] = [torch.empty(m, **f64) for _ in range(2)]
             T["cand_x"] = [torch.empty(na, **f64) for _ in range(2)]
             T["cand_z"] = [torch.empty(na, **f64) for _ in range(2)]
