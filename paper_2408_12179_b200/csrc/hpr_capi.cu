@@ -45,9 +45,9 @@ int fail(int code, const std::string &msg) {
       return fail(HPR_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));     \
   } while (0)
 
-#ifndef HPR_WIDE_MIN
-#define HPR_WIDE_MIN 1000000  // avg row length from which a lane keeps 8 entries in flight (measured: U=8 loses, 124 regs)
-#endif
+#ifndef HPR_GA_MIN
+#define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
+#endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
 constexpr int kPowBatch = 8;      // power steps per graph replay
 constexpr int kMaxGridPerSm = 8;  // CTAs per SM cap of the SELL kernels (partials sizing)
 constexpr int kSumsqBlocks = 1024;
@@ -212,7 +212,7 @@ struct hpr_ctx {
   Sell sa, sat;
   struct Cb {
     bool on = false;
-    int G = 0, NB = 0, rows_cap = 0, seg_cap = 0, smem = 0;
+    int G = 0, NB = 0, rows_cap = 0, seg_cap = 0, smem = 0, stages = 2;
     long long npad = 0, nrpb = 0;
     int *row_start = nullptr, *gstart = nullptr, *rpb = nullptr;
     long long *gseg = nullptr, *rpb_base = nullptr, *pos = nullptr;
@@ -236,13 +236,13 @@ struct hpr_ctx {
   long long launches = 0;
 
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
-    const int wide = S.nslices > 0 && S.slots >= (long long)HPR_WIDE_MIN * 32 * S.nslices;
+    const int ga = S.nslices > 0 && S.slots >= (long long)HPR_GA_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
-                   S.long_rows, S.nslices, S.nlong, wide};
+                   S.long_rows, S.nslices, S.nlong, ga};
   }
   CbMat cbmat(const Cb &C, int ncols) const {
     return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
-                 C.rows_cap, C.seg_cap};
+                 C.rows_cap, C.seg_cap, C.stages};
   }
   SellMat mat_a(bool scaled) const {
     return mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
@@ -256,18 +256,18 @@ namespace {
 
 // Launch the SELL kernel for epilogue Epi: grid = min(windows, occupancy x SMs);
 // returns the grid (= partials per quantity).
-template <int U, class Epi>
+template <int U, bool GA, class Epi>
 int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
                   int *grid_out) {
   static int occ = 0;
   if (occ == 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, Epi>, kThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, GA, Epi>, kThreads, 0));
     if (occ < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
     occ = std::min(occ, kMaxGridPerSm);
   }
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
-  k_sell<U, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
+  k_sell<U, GA, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
   CKL();
   c->launches += 1;
   if (grid_out) *grid_out = grid;
@@ -278,8 +278,8 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
 template <class Epi>
 int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
                 int *grid_out) {
-  return M.wide ? launch_sell_u<8>(c, M, xg, epi, part, grid_out)
-                : launch_sell_u<4>(c, M, xg, epi, part, grid_out);
+  return M.ga ? launch_sell_u<4, true>(c, M, xg, epi, part, grid_out)
+              : launch_sell_u<4, false>(c, M, xg, epi, part, grid_out);
 }
 
 // parts layout inside ctx->part (in doubles)
@@ -421,8 +421,10 @@ int cb_plan(hpr_ctx *c, const CbOff &o, const int *rp, const int *ci, int rows, 
   }
   for (long long q = 0; q < ng; ++q) C.seg_cap = (int)std::max<long long>(C.seg_cap, hseg[q + 1] - hseg[q]);
   C.npad = hseg[ng];
-  C.smem = cb_smem(kCbW, C.seg_cap, C.rows_cap).total;
-  C.on = C.smem <= kCbMaxSmem && C.npad < INT_MAX;
+  C.stages = kCbMaxStages;
+  while (C.stages > 2 && cb_smem(kCbW, C.seg_cap, C.rows_cap, C.stages).total > kCbMaxSmem) --C.stages;
+  C.smem = cb_smem(kCbW, C.seg_cap, C.rows_cap, C.stages).total;
+  C.on = C.smem <= kCbMaxSmem && C.npad < INT_MAX && C.rows_cap <= kCbMaxRpt * kCbThreads;
   return HPR_OK;
 }
 
@@ -460,17 +462,26 @@ int cb_layout(hpr_ctx *c, char *&p, hpr_ctx::Cb &C, const int *rp, const int *ci
   return HPR_OK;
 }
 
-template <class Epi>
-int launch_cb(hpr_ctx *c, const hpr_ctx::Cb &C, int ncols, const double *xg, const Epi &epi) {
-  static int smem_set = 0;
-  if (C.smem > smem_set) {
-    CK(cudaFuncSetAttribute(k_cb<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
-    smem_set = kCbMaxSmem;
+template <int RPT, class Epi>
+int launch_cb_r(hpr_ctx *c, const hpr_ctx::Cb &C, int ncols, const double *xg, const Epi &epi) {
+  static bool smem_set = false;
+  if (!smem_set) {
+    CK(cudaFuncSetAttribute(k_cb<RPT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
+    smem_set = true;
   }
-  k_cb<Epi><<<C.G, kCbThreads, C.smem, c->stream>>>(c->cbmat(C, ncols), xg, epi, nullptr);
+  k_cb<RPT, Epi><<<C.G, kCbThreads + 32, C.smem, c->stream>>>(c->cbmat(C, ncols), xg, epi, nullptr);
   CKL();
   c->launches += 1;
   return HPR_OK;
+}
+
+template <class Epi>
+int launch_cb(hpr_ctx *c, const hpr_ctx::Cb &C, int ncols, const double *xg, const Epi &epi) {
+  const int rpt = (C.rows_cap + kCbThreads - 1) / kCbThreads;
+  if (rpt <= 1) return launch_cb_r<1>(c, C, ncols, xg, epi);
+  if (rpt == 2) return launch_cb_r<2>(c, C, ncols, xg, epi);
+  if (rpt == 3) return launch_cb_r<3>(c, C, ncols, xg, epi);
+  return launch_cb_r<4>(c, C, ncols, xg, epi);
 }
 
 // fixed-order final reduction of a list of partial segments into ctx->results

@@ -25,8 +25,10 @@
 
 namespace hpr {
 
-constexpr int kCbThreads = 512;
-constexpr int kCbStages = 2;
+constexpr int kCbThreads = 512;      // consumer threads (+ one producer warp)
+constexpr int kCbWarps = kCbThreads / 32;
+constexpr int kCbMaxStages = 4;
+constexpr int kCbMaxRpt = 4;         // rows per consumer thread (register running sums)
 
 struct CbMat {
   const int *row_start;        // G + 1
@@ -38,6 +40,7 @@ struct CbMat {
   int G, NB, W, ncols;
   int rows_cap;                // >= max rows_g (shared-memory sizing)
   int seg_cap;                 // >= max padded group entries
+  int stages;                  // pipeline depth (2..kCbMaxStages)
 };
 
 struct CbSmem {                // byte offsets inside the dynamic shared memory
@@ -46,7 +49,7 @@ struct CbSmem {                // byte offsets inside the dynamic shared memory
 
 __host__ __device__ inline int cb_align16(int b) { return (b + 15) & ~15; }
 
-__host__ __device__ inline CbSmem cb_smem(int W, int seg_cap, int rows_cap) {
+__host__ __device__ inline CbSmem cb_smem(int W, int seg_cap, int rows_cap, int stages) {
   CbSmem s;
   const int w = W * 8, v = seg_cap * 8, c = cb_align16(seg_cap * 2), r = cb_align16((rows_cap + 1) * 4);
   s.stage_bytes = w + v + c + r;
@@ -54,8 +57,8 @@ __host__ __device__ inline CbSmem cb_smem(int W, int seg_cap, int rows_cap) {
   s.sval = w;
   s.sci = w + v;
   s.srpb = w + v + c;
-  s.rs = kCbStages * s.stage_bytes;
-  s.total = s.rs + cb_align16(rows_cap * 8);
+  s.rs = stages * s.stage_bytes;
+  s.total = s.rs;
   return s;
 }
 
@@ -67,70 +70,92 @@ __device__ __forceinline__ void bulk_g2s_nohint(void *dst, const void *src, uint
       : "memory");
 }
 
-template <class Epi>
-__global__ void __launch_bounds__(kCbThreads, 1)
+// Warp-specialised pipeline: warp kCbWarps (the producer) issues the bulk copies
+// of block b into stage b % S as soon as every consumer warp has released that
+// stage (per-stage "empty" mbarriers); the consumer warps wait on the stage's
+// "full" mbarrier, add their rows' products into REGISTER running sums (RPT
+// rows per thread) and release it -- no CTA-wide barrier in the loop.
+template <int RPT, class Epi>
+__global__ void __launch_bounds__(kCbThreads + 32, 1)
 k_cb(CbMat M, const double *__restrict__ xg, Epi epi, double *part) {
   extern __shared__ __align__(128) unsigned char cbsm[];
-  __shared__ uint64_t bar[kCbStages];
+  __shared__ uint64_t full[kCbMaxStages], empty[kCbMaxStages];
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll
   for (int q = 0; q < (Epi::NQ > 0 ? Epi::NQ : 1); ++q) acc[q] = 0.0;
   if (!epi.enter()) return;
   const int g = blockIdx.x, tid = threadIdx.x;
   const int r0 = M.row_start[g], rows = M.row_start[g + 1] - r0;
-  const CbSmem L = cb_smem(M.W, M.seg_cap, M.rows_cap);
-  double *rs = (double *)(cbsm + L.rs);
+  const int S = M.stages;
+  const CbSmem L = cb_smem(M.W, M.seg_cap, M.rows_cap, S);
   if (tid == 0) {
-    for (int s = 0; s < kCbStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCbWarps);
+    }
     fence_mbar_init();
   }
-  for (int i = tid; i < rows; i += kCbThreads) rs[i] = 0.0;
   __syncthreads();
-  auto issue = [&](int b) {
-    const int st = b % kCbStages;
-    unsigned char *base = cbsm + st * L.stage_bytes;
-    const long long q = (long long)g * M.NB + b;
-    const long long e0 = M.gseg[q], e1 = M.gseg[q + 1];
-    const int wcols = min(M.W, M.ncols - b * M.W);
-    const uint32_t wb = (uint32_t)cb_align16(wcols * 8);
-    const uint32_t vb = (uint32_t)((e1 - e0) * 8);                 // e1 - e0: multiple of 8
-    const uint32_t cb = (uint32_t)((e1 - e0) * 2);
-    const uint32_t rb = (uint32_t)cb_align16((rows + 1) * 4);
-    mbar_expect_tx(&bar[st], wb + vb + cb + rb);
-    bulk_g2s_nohint(base + L.wbuf, xg + (long long)b * M.W, wb, &bar[st]);
-    if (vb) {
-      bulk_g2s_nohint(base + L.sval, M.val + e0, vb, &bar[st]);
-      bulk_g2s_nohint(base + L.sci, M.ci + e0, cb, &bar[st]);
+  if (tid >= kCbThreads) {                       // producer warp
+    if (tid == kCbThreads) {
+      for (int b = 0; b < M.NB; ++b) {
+        const int st = b % S;
+        if (b >= S) mbar_wait(&empty[st], (uint32_t)(((b / S) - 1) & 1));
+        unsigned char *base = cbsm + st * L.stage_bytes;
+        const long long q = (long long)g * M.NB + b;
+        const long long e0 = M.gseg[q], e1 = M.gseg[q + 1];
+        const int wcols = min(M.W, M.ncols - b * M.W);
+        const uint32_t wb = (uint32_t)cb_align16(wcols * 8);
+        const uint32_t vb = (uint32_t)((e1 - e0) * 8);            // e1 - e0: multiple of 8
+        const uint32_t cb = (uint32_t)((e1 - e0) * 2);
+        const uint32_t rb = (uint32_t)cb_align16((rows + 1) * 4);
+        mbar_expect_tx(&full[st], wb + vb + cb + rb);
+        bulk_g2s_nohint(base + L.wbuf, xg + (long long)b * M.W, wb, &full[st]);
+        if (vb) {
+          bulk_g2s_nohint(base + L.sval, M.val + e0, vb, &full[st]);
+          bulk_g2s_nohint(base + L.sci, M.ci + e0, cb, &full[st]);
+        }
+        bulk_g2s_nohint(base + L.srpb, M.rpb + M.rpb_base[q], rb, &full[st]);
+      }
     }
-    bulk_g2s_nohint(base + L.srpb, M.rpb + M.rpb_base[q], rb, &bar[st]);
-  };
-  if (tid == 0)
-    for (int b = 0; b < kCbStages && b < M.NB; ++b) issue(b);
+    return;
+  }
+  double rs[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) rs[j] = 0.0;
   for (int b = 0; b < M.NB; ++b) {
-    const int st = b % kCbStages;
-    mbar_wait(&bar[st], (uint32_t)((b / kCbStages) & 1));
+    const int st = b % S;
+    mbar_wait(&full[st], (uint32_t)((b / S) & 1));
     const unsigned char *base = cbsm + st * L.stage_bytes;
     const double *wv = (const double *)(base + L.wbuf);
     const double *sv = (const double *)(base + L.sval);
     const unsigned short *sc = (const unsigned short *)(base + L.sci);
     const int *sr = (const int *)(base + L.srpb);
-    for (int i = tid; i < rows; i += kCbThreads) {
-      double s = rs[i];
-      const int k1 = sr[i + 1];
-      for (int k = sr[i]; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(sv[k], wv[sc[k]]));
-      rs[i] = s;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int i = tid + j * kCbThreads;
+      if (i < rows) {
+        double s = rs[j];
+        const int k1 = sr[i + 1];
+        for (int k = sr[i]; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(sv[k], wv[sc[k]]));
+        rs[j] = s;
+      }
     }
-    __syncthreads();                     // stage st consumed by every thread
-    if (tid == 0 && b + kCbStages < M.NB) {
-      fence_proxy_async();               // generic-proxy reads before the async-proxy refill
-      issue(b + kCbStages);
+    __syncwarp();
+    if ((tid & 31) == 0) {
+      fence_proxy_async();                       // generic reads before the async refill
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
     }
   }
-  for (int i = tid; i < rows; i += kCbThreads) {
-    epi.prefetch(r0 + i);
-    epi.finish(r0 + i, rs[i], acc);
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int i = tid + j * kCbThreads;
+    if (i < rows) {
+      epi.prefetch(r0 + i);
+      epi.finish(r0 + i, rs[j], acc);
+    }
   }
-  if constexpr (Epi::NQ > 0) block_reduce_store<Epi::NQ>(acc, part, gridDim.x);
+  if constexpr (Epi::NQ > 0) static_assert(Epi::NQ == 0, "CB engine: iteration epilogues only");
 }
 
 // ---- layout construction (hpr_analyze) ----

@@ -75,7 +75,7 @@ struct SellMat {
   const int *long_rows;
   int nslices;
   int nlong;
-  int wide;                // long rows: 8 entries per lane in flight (HPR_WIDE_MIN)
+  int ga;                  // long rows: gather one batch ahead (HPR_GA_MIN)
 };
 
 constexpr int kSlice = 32;
@@ -85,9 +85,7 @@ constexpr int kWarpsPerCta = kThreads / 32;
 #ifndef HPR_UNROLL
 #define HPR_UNROLL 4
 #endif
-#ifndef HPR_GATHER_AHEAD
-#define HPR_GATHER_AHEAD 0
-#endif
+
 constexpr int kUnroll = HPR_UNROLL;     // entries per lane in flight (x2: software pipelined)
 
 // Parameters of the inner iterations, resident in device memory so a captured
@@ -167,7 +165,7 @@ __device__ __forceinline__ SliceHdr load_hdr(const SellMat &M, int s, int lane) 
   return h;
 }
 
-template <int U, class Epi>
+template <int U, bool GA, class Epi>
 __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
@@ -186,7 +184,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       c[u] = ld_stream(cp + u * kSlice, pol);
       v[u] = ld_stream(vp + u * kSlice, pol);
     }
-#if HPR_GATHER_AHEAD
+  if constexpr (GA) {
   // depth-2 pipeline: batch k+1's operand gathers and batch k+2's matrix loads
   // are in flight while batch k's products are added (long rows: the gather
   // latency is exposed once per two batches instead of once per batch)
@@ -226,8 +224,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       v1[u] = v2[u];
     }
   }
-  if (false)
-#endif
+  } else {
   for (int k = 0; k < slen; k += U) {
     int cn[U];
     double vn[U], xv[U];
@@ -248,6 +245,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       c[u] = cn[u];
       v[u] = vn[u];
     }
+  }
   }
   if (row >= 0) epi.finish(row, sum, acc);
 }
@@ -324,7 +322,7 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
 #ifndef HPR_SELL_MINB
 #define HPR_SELL_MINB 1      // min resident CTAs per SM requested from ptxas (register cap)
 #endif
-template <int U, class Epi>
+template <int U, bool GA, class Epi>
 __global__ void __launch_bounds__(kThreads, HPR_SELL_MINB)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
@@ -341,7 +339,7 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
     SliceHdr h = load_hdr(M, blockIdx.x * kWarpsPerCta + wib, lane);
     for (int win = blockIdx.x; win < nwin; win += G) {
       const SliceHdr hn = load_hdr(M, (win + G) * kWarpsPerCta + wib, lane);
-      sell_slice<U>(M, h, lane, xg, epi, acc, pol);
+      sell_slice<U, GA>(M, h, lane, xg, epi, acc, pol);
       h = hn;
     }
   }
