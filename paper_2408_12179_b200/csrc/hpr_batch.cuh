@@ -87,18 +87,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // sequential sum of row r of a shared-memory CSR against vector v
 __device__ __forceinline__ double srow(const int *rp, const int *ci, const double *val,
                                        const double *v, int r) {
-  // products four at a time (independent shared-memory loads in flight), added
-  // strictly left to right -- the same rounding sequence as a plain loop
   double s = 0.0;
   int e = rp[r];
   const int e1 = rp[r + 1];
-  for (; e + 3 < e1; e += 4) {
-    const double p0 = __dmul_rn(val[e], v[ci[e]]);
-    const double p1 = __dmul_rn(val[e + 1], v[ci[e + 1]]);
-    const double p2 = __dmul_rn(val[e + 2], v[ci[e + 2]]);
-    const double p3 = __dmul_rn(val[e + 3], v[ci[e + 3]]);
-    s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
-  }
   for (; e < e1; ++e) s = __dadd_rn(s, __dmul_rn(val[e], v[ci[e]]));
   return s;
 }

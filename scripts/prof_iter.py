@@ -30,3 +30,5 @@ per_it = min(times) / a.steps
 bi = b_iter(dev.m, dev.n, dev.nnz)
 print(f"{a.config}: m={dev.m} n={dev.n} nnz={dev.nnz} layout={dev.layout_info()} gen={tg:.1f}s analyze={ta*1e3:.1f}ms scale={ts*1e3:.1f}ms power={tp*1e3:.1f}ms ({est.iterations} it)")
 print(f"per-iteration {per_it*1e6:.2f} us  (median {np.median(times)/a.steps*1e6:.2f})  B_iter={bi/1e6:.1f} MB  -> {bi/per_it/1e9:.1f} GB/s")
+import subprocess
+print("clocks:", subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks.mem,power.draw,clocks_event_reasons.active", "--format=csv,noheader"], capture_output=True, text=True).stdout.strip())
