@@ -323,6 +323,49 @@ int hpr_batch_solve(const hpr_batch_problem *p, const hpr_batch_config *cfg, voi
                     size_t ws_bytes, hpr_batch_result *results, hpr_restart_rec *log,
                     double *x, double *y, double *z, int device, void *stream);
 
+/* ------------------------------------------------------------------------
+ * MPS reader / writer (host code) with the semantics of
+ * the reference's mps.py (read_document 60-154, document_to_problem 157-278,
+ * write_mps 295-364): standard minimisation form, equality rows first, then
+ * >= rows (L rows negated, RANGES split), OBJSENSE MAX negates c.
+ * ------------------------------------------------------------------------ */
+typedef struct hpr_mps_result {
+  int64_t m1, m2, n;
+  int64_t *eq_rp, *eq_ci;       /* m1 + 1, nnz: canonical CSR of the equality block */
+  double *eq_val;
+  int64_t *in_rp, *in_ci;       /* m2 + 1, nnz: the >= block */
+  double *in_val;
+  double *b_eq, *b_ineq, *c, *lower, *upper;
+  double objective_constant;
+  int32_t objective_negated;
+  int32_t extra_objective_rows; /* N rows after the first (dropped; the caller warns) */
+  char *row_names;              /* m1 + m2 NUL-terminated names, back to back */
+  char *col_names;              /* n names */
+  char *name;                   /* NAME section */
+} hpr_mps_result;
+
+/* HPR_EINVAL on a malformed file: hpr_mps_last_error() = "line N: message". */
+int hpr_mps_parse(const char *text, size_t len, hpr_mps_result **out);
+const char *hpr_mps_last_error(void);
+int hpr_mps_free(hpr_mps_result *r);
+
+typedef struct hpr_mps_problem {
+  int64_t m1, m2, n;
+  const int64_t *eq_rp, *eq_ci;
+  const double *eq_val;
+  const int64_t *in_rp, *in_ci;
+  const double *in_val;
+  const double *b_eq, *b_ineq, *c, *lower, *upper;
+  double objective_constant;
+  int32_t objective_negated;
+  const char *row_names;        /* NULL: EQ<i> / GE<i> */
+  const char *col_names;        /* NULL: X<j> */
+} hpr_mps_problem;
+
+/* *text is malloc'ed (release with hpr_mps_free_text). */
+int hpr_mps_write(const hpr_mps_problem *p, const char *name, char **text, size_t *len);
+int hpr_mps_free_text(char *text);
+
 #ifdef __cplusplus
 }
 #endif

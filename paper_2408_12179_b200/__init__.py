@@ -11,6 +11,7 @@ from .driver import (KktResidual, RestartEvent, RestartKind, SolveReport, Solver
                      SolveStatus, Timings, Variant, check_restart, check_termination,
                      kkt_residual, sigma_guards_pass, solve)
 from .generators import generate_flow_lp, generate_known_solution_lp, generate_planted_lp_fast
+from .mps import MpsParseError, load_mps, parse_mps, write_mps
 from .problem import (DimensionMismatchError, LpProblem, PrimalDualPoint, SparseMatrix,
                       dual_objective, primal_objective, project_onto_box,
                       project_onto_dual_cone)
@@ -18,7 +19,8 @@ from .problem import (DimensionMismatchError, LpProblem, PrimalDualPoint, Sparse
 __version__ = "0.1.0"
 
 __all__ = [
-    "DimensionMismatchError", "KktResidual", "LpProblem", "PrimalDualPoint", "RestartEvent",
+    "DimensionMismatchError", "KktResidual", "LpProblem", "MpsParseError", "load_mps",
+    "parse_mps", "write_mps", "PrimalDualPoint", "RestartEvent",
     "RestartKind", "SolveReport", "SolveStatus", "SolverConfig", "SparseMatrix", "Timings",
     "Variant", "check_restart", "check_termination", "dual_objective",
     "generate_flow_lp", "generate_known_solution_lp", "generate_planted_lp_fast",

@@ -191,6 +191,13 @@ _SIGS = {
                                        ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_int, ctypes.c_void_p]),
+    # MPS reader / writer (hpr_mps.cpp; typed precisely by paper_2408_12179_b200.mps)
+    "hpr_mps_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "hpr_mps_last_error": (ctypes.c_char_p, []),
+    "hpr_mps_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_mps_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p,
+                                     ctypes.c_void_p]),
+    "hpr_mps_free_text": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu")]
+SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu"), os.path.join(HERE, "csrc", "hpr_mps.cpp")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
               os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
               os.path.join(HERE, "csrc", "hpr_batch.cuh"),
