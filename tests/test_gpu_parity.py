@@ -287,3 +287,15 @@ def test_kkt_residual_vs_oracle():
     ref = O.kkt(O.OracleLP.from_problem(prob), pt.y, pt.z, pt.x)
     for k, v in ref.items():
         assert _close(got[k], v, 1e-12), k
+
+
+def test_mps_round_trip_solve_bit_for_bit():
+    """reference test_mps.py:184-192 on the GPU path: a problem and its MPS
+    round trip (native reader/writer) solve to identical reports and points."""
+    prob, _ = P.generate_known_solution_lp(5, 4, 3, 15, 0.4)
+    back = P.parse_mps(P.write_mps(prob))
+    a = P.solve(prob, P.SolverConfig(tolerance=1e-8))
+    b = P.solve(back, P.SolverConfig(tolerance=1e-8))
+    assert a.iterations == b.iterations
+    assert a.primal_objective == b.primal_objective
+    assert np.array_equal(a.solution.x, b.solution.x)
