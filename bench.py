@@ -360,9 +360,12 @@ def run_ours(args):
     t_max, its_all = _max_sum(dist, local, total_ms / 1e3, its_total)
     value = its_all / t_max
 
-    # e2e through the public API from host arrays (upload + solve + D2H solution)
+    # e2e through the public API from host arrays: every step uploads the
+    # problem (pinned staging -> H2D), re-analyses it, solves and copies the
+    # solution back; one untimed call first warms the device-residency pool
     e2e_its, e2e_t = 0, 0.0
     h2d = d2h = 0
+    P.solve(prob, cfg, device=local)
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()

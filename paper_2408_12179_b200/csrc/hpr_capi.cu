@@ -45,6 +45,9 @@ int fail(int code, const std::string &msg) {
       return fail(HPR_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));     \
   } while (0)
 
+#ifndef HPR_PDL
+#define HPR_PDL 1       // programmatic dependent launch between the inner-loop phases
+#endif
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
@@ -231,6 +234,7 @@ struct hpr_ctx {
   PowState *h_pow = nullptr;         // pinned
   std::map<int, cudaGraphExec_t> inner_graphs;
   cudaGraphExec_t pow_graph = nullptr;
+  std::vector<long long> graph_sig;   // layout identity the graphs were captured against
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   bool inner_timed = false, ckpt_timed = false;
   long long launches = 0;
@@ -258,7 +262,7 @@ namespace {
 // returns the grid (= partials per quantity).
 template <int U, bool GA, class Epi>
 int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
-                  int *grid_out) {
+                  int *grid_out, bool pdl) {
   static int occ = 0;
   if (occ == 0) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, GA, Epi>, kThreads, 0));
@@ -267,7 +271,20 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
   }
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
-  k_sell<U, GA, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
+  if (pdl && HPR_PDL) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_sell<U, GA, Epi>, M, xg, epi, part));
+  } else {
+    k_sell<U, GA, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
+  }
   CKL();
   c->launches += 1;
   if (grid_out) *grid_out = grid;
@@ -277,9 +294,9 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
 // entries in flight per lane follow the matrix's average row length
 template <class Epi>
 int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
-                int *grid_out) {
-  return M.ga ? launch_sell_u<4, true>(c, M, xg, epi, part, grid_out)
-              : launch_sell_u<4, false>(c, M, xg, epi, part, grid_out);
+                int *grid_out, bool pdl = false) {
+  return M.ga ? launch_sell_u<4, true>(c, M, xg, epi, part, grid_out, pdl)
+              : launch_sell_u<4, false>(c, M, xg, epi, part, grid_out, pdl);
 }
 
 // parts layout inside ctx->part (in doubles)
@@ -672,6 +689,7 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
     cudaGraphExecDestroy(c->pow_graph);
     c->pow_graph = nullptr;
   }
+  c->graph_sig.clear();
   c->bound = true;
   c->analyzed = c->laid_out = c->scaled = false;
   return HPR_OK;
@@ -746,11 +764,24 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   rc = cb_layout(c, p, c->cbat, B.at_rp, B.at_ci);
   if (rc) return rc;
   CK(cudaStreamSynchronize(c->stream));
-  for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
-  c->inner_graphs.clear();
-  if (c->pow_graph) {
-    cudaGraphExecDestroy(c->pow_graph);
-    c->pow_graph = nullptr;
+  // the captured graphs hold the layout's pointers and the plans' counts: keep
+  // them when a re-analysed problem reproduces both (a re-solve of the same
+  // structure), drop them otherwise
+  std::vector<long long> sig = {(long long)(uintptr_t)layout, (long long)bytes};
+  for (const Sell *S : {&c->sa, &c->sat})
+    for (long long v : {(long long)S->nslices, S->slots, (long long)S->nlong}) sig.push_back(v);
+  for (const hpr_ctx::Cb *C : {&c->cba, &c->cbat})
+    for (long long v : {(long long)C->on, (long long)C->G, (long long)C->NB, (long long)C->rows_cap,
+                        (long long)C->seg_cap, (long long)C->stages, C->npad, C->nrpb})
+      sig.push_back(v);
+  if (sig != c->graph_sig) {
+    for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
+    c->inner_graphs.clear();
+    if (c->pow_graph) {
+      cudaGraphExecDestroy(c->pow_graph);
+      c->pow_graph = nullptr;
+    }
+    c->graph_sig = sig;
   }
   c->laid_out = true;
   c->scaled = false;
@@ -1025,11 +1056,12 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     for (int i = 0; i < steps; ++i) {
       ex.step = i;
       ey.step = i;
+      // the first kernel of the graph follows the k_set_params launch: plain edge
       int rc2 = c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
-                           : launch_sell(c, AT, B.y, ex, nullptr, nullptr);
+                           : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
       if (!rc2)
         rc2 = c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
-                        : launch_sell(c, A, B.w, ey, nullptr, nullptr);
+                        : launch_sell(c, A, B.w, ey, nullptr, nullptr, true);
       if (rc2) {
         cudaStreamEndCapture(s, &g);
         return rc2;

@@ -335,8 +335,13 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   const int G = gridDim.x;
   // the next window's slice header is loaded while this one is processed, so
   // a slice costs two dependent memory round trips (matrix, gather), not three
+  // programmatic dependent launch (inner-loop graph): let the next phase's CTAs
+  // be scheduled as this grid drains; only the static slice header is read
+  // before the previous phase's results (gathered vector, iterates) are waited for
+  asm volatile("griddepcontrol.launch_dependents;");
   {
     SliceHdr h = load_hdr(M, blockIdx.x * kWarpsPerCta + wib, lane);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int win = blockIdx.x; win < nwin; win += G) {
       const SliceHdr hn = load_hdr(M, (win + G) * kWarpsPerCta + wib, lane);
       sell_slice<U, GA>(M, h, lane, xg, epi, acc, pol);

@@ -91,6 +91,27 @@ class DeviceLP:
         self._setup(parts, m, n, m1, (problem.b_eq, problem.b_ineq), problem.c, problem.lower,
                     problem.upper, device=device, stream=stream)
 
+    def dims_key(self):
+        return (self.device.index, self.m, self.n, self.m1, self.nnz, self.n_alloc)
+
+    @staticmethod
+    def problem_key(problem, device: int):
+        top, bot = problem.a_eq, problem.a_ineq
+        n = int(top.ncols)
+        nnz = int(top.row_offsets[-1]) - int(top.row_offsets[0]) + \
+            int(bot.row_offsets[-1]) - int(bot.row_offsets[0])
+        return (device, int(top.nrows) + int(bot.nrows), n, int(top.nrows), nnz, n)
+
+    def reload(self, problem):
+        """Upload another problem of identical dimensions into these buffers
+        (inputs are re-copied and re-analysed; the context, the workspace and,
+        when the layout comes out identical, the captured graphs are reused)."""
+        if DeviceLP.problem_key(problem, self.device.index) != self.dims_key():
+            raise ValueError("reload needs a problem of identical dimensions")
+        self._setup(_csr_parts(problem), self.m, self.n, self.m1,
+                    (problem.b_eq, problem.b_ineq), problem.c, problem.lower, problem.upper,
+                    device=self.device.index, stream=self.stream, n_alloc=self.n_alloc)
+
     @classmethod
     def from_arrays(cls, ro, ci, v, m, n, m1, b, c, lower, upper, *, device: int = 0,
                     stream=None, n_alloc: int | None = None, pinned_upload: bool = True):
@@ -161,15 +182,21 @@ class DeviceLP:
             offs.append(total)
             total += (ln * np.dtype(dt).itemsize + 255) // 256 * 256
         T = {}
+        if getattr(self, "_inputs", None) is None or self._inputs.numel() != total:
+            with torch.cuda.stream(self.stream):
+                self._inputs = torch.empty(total, dtype=torch.uint8, device=dev)
         with _Staging.lock:
             stage = _Staging.get(total)
             host = stage.numpy()
             for (name, dt, ln, fill), o in zip(spec, offs):
                 fill(host[o:o + ln * np.dtype(dt).itemsize].view(dt))
             with torch.cuda.stream(self.stream):
-                self._inputs = torch.empty(total, dtype=torch.uint8, device=dev)
                 self._inputs.copy_(stage[:total], non_blocking=True)
             self.stream.synchronize()       # the staging buffer is reusable after this
+        if getattr(self, "ctx", None) is not None:
+            self.h2d_bytes = total
+            self.analyzed = False           # a reload: same buffers, new contents
+            return
         tdt = {np.int32: torch.int32, np.float64: torch.float64}
         for (name, dt, ln, _), o in zip(spec, offs):
             T[name] = self._inputs[o:o + ln * np.dtype(dt).itemsize].view(tdt[dt])
@@ -219,9 +246,10 @@ class DeviceLP:
         torch = _torch()
         nbytes = ctypes.c_size_t(0)
         N.call("hpr_analyze", self.ctx, ctypes.byref(nbytes))
-        with torch.cuda.stream(self.stream):
-            self.layout = torch.empty(max(int(nbytes.value), 16), dtype=torch.uint8,
-                                      device=self.device)
+        need = max(int(nbytes.value), 16)
+        if getattr(self, "layout", None) is None or self.layout.numel() != need:
+            with torch.cuda.stream(self.stream):
+                self.layout = torch.empty(need, dtype=torch.uint8, device=self.device)
         N.call("hpr_bind_layout", self.ctx, ctypes.c_void_p(self.layout.data_ptr()),
                ctypes.c_size_t(self.layout.numel()))
         self.analyzed = True

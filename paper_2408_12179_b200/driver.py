@@ -294,22 +294,81 @@ def merit_from_sums(o, sigma, lam) -> float:
 # solve
 # ---------------------------------------------------------------------------
 
+class _DevicePool:
+    """Device residencies kept between solve() calls, keyed by the problem's
+    dimensions (like an FFT plan cache): a later problem of the same shape is
+    uploaded into the same buffers and context, so its solve skips the device
+    allocations and -- when its structure reproduces the layout -- the CUDA
+    graph captures.  Inputs are always re-uploaded and re-analysed.  An entry
+    is checked out for the duration of a solve, so concurrent solves never
+    share one."""
+
+    def __init__(self, capacity: int = 2, max_bytes: float = 4e9):
+        import threading
+        self.capacity = capacity
+        self.max_bytes = max_bytes
+        self.free: list[DeviceLP] = []
+        self.lock = threading.Lock()
+
+    def acquire(self, problem, device: int) -> DeviceLP:
+        key = DeviceLP.problem_key(problem, device)
+        with self.lock:
+            for i, d in enumerate(self.free):
+                if d.dims_key() == key:
+                    dev = self.free.pop(i)
+                    break
+            else:
+                dev = None
+        if dev is None:
+            return DeviceLP(problem, device=device)
+        dev.reload(problem)
+        return dev
+
+    def release(self, dev: DeviceLP):
+        if 92 * dev.nnz + 160 * (dev.m + dev.n) > self.max_bytes:
+            dev.close()                       # large residencies are not kept
+            return
+        with self.lock:
+            self.free.insert(0, dev)
+            while len(self.free) > self.capacity:
+                self.free.pop().close()
+
+    def clear(self):
+        with self.lock:
+            for d in self.free:
+                d.close()
+            self.free.clear()
+
+
+DEVICE_POOL = _DevicePool()
+
+
 def solve(problem, cfg=None, *, device: int = 0, dev: DeviceLP | None = None) -> SolveReport:
     """Run the restarted HPR-LP solver on the GPU (reference driver.py:281-405).
 
     ``problem``: our ``LpProblem`` or the reference's (duck-typed).
     ``dev``: an already-uploaded ``DeviceLP`` of this problem (re-solves skip
-    the upload; the state is reset).
+    the upload; the state is reset).  Without it the problem is uploaded into
+    a pooled device residency (``DEVICE_POOL``).
     """
+    if dev is not None:
+        return _solve(problem, cfg, dev)
+    dev = DEVICE_POOL.acquire(problem, device)
+    try:
+        return _solve(problem, cfg, dev)
+    finally:
+        DEVICE_POOL.release(dev)
+
+
+def _solve(problem, cfg, dev) -> SolveReport:
     cfg = SolverConfig.coerce(cfg)
     wall_start = time.perf_counter()
+    launches0 = dev.launch_count()
     timings = Timings()
     variant = cfg.variant
     vcode = N.VARIANT_CODE[variant.value]
 
     t0 = time.perf_counter()
-    if dev is None:
-        dev = DeviceLP(problem, device=device)
     if not dev.analyzed:
         dev.analyze()
     if dev.nnz == 0:
@@ -417,7 +476,7 @@ def solve(problem, cfg=None, *, device: int = 0, dev: DeviceLP | None = None) ->
         sigma_final=sigma, lambda_estimate=lam,
         device_stats={"lambda_raw": est.raw, "power_iterations": est.iterations,
                       "b_factor": sc.b_factor, "c_factor": sc.c_factor,
-                      "launches": dev.launch_count(), "layout": layout,
+                      "launches": dev.launch_count() - launches0, "layout": layout,
                       "h2d_bytes": dev.h2d_bytes})
 
 
