@@ -27,6 +27,7 @@ namespace hpr {
 namespace batch {
 
 constexpr int kBT = 512;            // threads per CTA (one LP)
+constexpr int kWTab = 256;          // Halpern weights tabulated per refill
 constexpr int kBW = kBT / 32;
 
 struct Prob {
@@ -112,6 +113,7 @@ size_t smem_bytes(int m, int n, long long nnz) {
   b += 4 * (size_t)(m + 1 + n + 1);            // arp, atrp
   b = (b + 15) / 16 * 16;
   b += 8 * (size_t)24 * kBW;                   // reduction scratch
+  b += 16 * (size_t)kWTab;                     // Halpern weight table
   return b;
 }
 
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   int *arp = ip; ip += m + 1;
   int *atrp = ip; ip += n + 1;
   double *red = (double *)(((uintptr_t)ip + 15) & ~(uintptr_t)15);
+  double *wtab = red + 24 * kBW;
   // global views of this LP
   const int *grp = P.rp + r0 + lp;             // local row pointers (m + 1)
   const int *gci = P.ci + z0;
@@ -382,9 +385,18 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     const long long steps = C.max_iter - k < C.check_interval ? C.max_iter - k : C.check_interval;
     const double lamsig = lamv * sigma;
     bool broke = false;
+    const long long t_seg = t;
     for (long long st = 0; st < steps; ++st) {
-      const double t2 = (double)t + 2.0;
-      const double wn = ((double)t + 1.0) / t2, wa = 1.0 / t2;
+      if (st % kWTab == 0) {                     // Halpern weights of the next kWTab steps
+        for (int q = tid; q < kWTab; q += kBT) {
+          const double tq = (double)(t_seg + st + q);
+          const double t2 = tq + 2.0;            // core.py:142-144
+          wtab[2 * q] = (tq + 1.0) / t2;
+          wtab[2 * q + 1] = 1.0 / t2;
+        }
+        __syncthreads();
+      }
+      const double wn = wtab[2 * (st % kWTab)], wa = wtab[2 * (st % kWTab) + 1];
       int bad = 0;
       for (int j = tid; j < n; j += kBT) {       // x phase (core.py:168-169)
         const double aty = srow(atrp, atci, atv, y, j);

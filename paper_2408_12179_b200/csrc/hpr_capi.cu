@@ -46,7 +46,7 @@ int fail(int code, const std::string &msg) {
   } while (0)
 
 #ifndef HPR_PDL
-#define HPR_PDL 1       // programmatic dependent launch between the inner-loop phases
+#define HPR_PDL 0       // programmatic dependent launch between inner-loop phases (measured: no gain in graphs)
 #endif
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
