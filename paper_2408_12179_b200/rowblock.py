@@ -185,6 +185,8 @@ class RowBlockGroup:
         return out
 
     def launch_count(self) -> int:
+        if self.g is None:
+            return 0
         v = ctypes.c_int64(0)
         N.call("hpr_group_launch_count", self.g, ctypes.byref(v))
         return int(v.value)
