@@ -211,10 +211,12 @@ int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);
  * Each rank is an ordinary hpr_ctx created for its row block: dims
  * (m_g, n, m1_g, nnz_g) with A_g = the block's rows (all n columns), bound
  * with buffers whose column-indexed arrays (c, lower, upper, *_s, col_scale,
- * x, anc_x, w, xb, zb, wtmp, cand_x, cand_z) hold n_pad = P*ceil(n/P)
- * doubles, then hpr_analyze + hpr_bind_layout as usual.  The group then takes
- * over: scale / power / run_inner / checkpoint / restart / finalize below.
- * Rank g owns the column slice [g*ceil(n/P), min((g+1)*ceil(n/P), n)).
+ * x, anc_x, w, xb, zb, wtmp, cand_x, cand_z) hold npad doubles
+ * (hpr_group_dims), then hpr_analyze + hpr_bind_layout as usual.  The group
+ * then takes over: scale / power / run_inner / checkpoint / restart / finalize.
+ * Columns are split into `chunks` chunks of nranks slices of cw columns; rank
+ * g owns slice g of every chunk.  With NCCL and chunks > 1 the inner loop
+ * overlaps chunk q's collectives with the partial SpMV of chunk q+1.
  *
  * Transports:
  *   nccl_id != NULL: NCCL, one local rank per process (nlocal = 1), rank0 =
@@ -229,14 +231,16 @@ typedef struct hpr_group hpr_group;
 int hpr_nccl_available(void);
 int hpr_nccl_unique_id(void *id, size_t bytes);          /* bytes >= 128 */
 
-/* per-rank row-block workspace (partials, reduced slice, gathered scalars) */
-int hpr_group_ws_bytes(int64_t n, int nranks, size_t *bytes);
+/* padded column length and per-rank row-block workspace (partials, reduced
+ * owned entries, gathered scalars) for n columns over nranks ranks */
+int hpr_group_dims(int64_t n, int nranks, int chunks, int64_t *npad, size_t *ws_bytes);
 
 int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *const *rb_ws,
-                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0,
+                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0, int chunks,
                      const void *nccl_id, size_t id_bytes);
 int hpr_group_destroy(hpr_group *g);
-int hpr_group_col_range(hpr_group *g, int local, int64_t *j0, int64_t *j1);
+/* rank g owns columns q*nranks*cw + g*cw + [0, cw) for q < chunks */
+int hpr_group_col_layout(hpr_group *g, int64_t *chunks, int64_t *cw, int64_t *npad);
 
 /* scale_problem (scaling.py:72-125): Ruiz column maxima all-reduced (MAX),
  * Pock-Chambolle column sums all-reduced (SUM), norms summed over ranks. */

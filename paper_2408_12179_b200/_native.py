@@ -148,18 +148,19 @@ _SIGS = {
     # row-block partitioned mode (hpr_rowblock.cuh)
     "hpr_nccl_available": (ctypes.c_int, []),
     "hpr_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
-    "hpr_group_ws_bytes": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int,
-                                          ctypes.POINTER(ctypes.c_size_t)]),
+    "hpr_group_dims": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_size_t)]),
     "hpr_group_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_int64), ctypes.c_size_t,
-                                        ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
-                                        ctypes.c_size_t]),
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_size_t]),
     "hpr_group_destroy": (ctypes.c_int, [ctypes.c_void_p]),
-    "hpr_group_col_range": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
-                                           ctypes.POINTER(ctypes.c_int64),
-                                           ctypes.POINTER(ctypes.c_int64)]),
+    "hpr_group_col_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.POINTER(ctypes.c_int64)]),
     "hpr_group_scale": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.POINTER(HprScaleOut)]),
     "hpr_group_power": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int,

@@ -5,19 +5,23 @@
 // of the stacked rows of A (balanced by nonzeros), i.e. an ordinary hpr_ctx
 // whose dims are (m_g, n, m1_g, nnz_g): A_g is m_g x n and its transpose A_g^T
 // is n x m_g.  Everything row-indexed (y, b, anchors, row scale) is local.
-// Column-indexed vectors are allocated at length n_pad = P * cnt on every rank
-// (cnt = ceil(n / P)); rank g owns the column slice [g*cnt, min((g+1)*cnt, n)).
+// Column-indexed vectors are allocated at length npad on every rank; the
+// columns are split into K chunks of P slices of cw columns and rank g owns
+// slice g of every chunk (hpr_group_dims / hpr_group_col_layout).
 //
 // One inner iteration (core.py:168-172):
 //   p_g   = A_g^T y_g                        SELL kernel, n partial outputs
-//   aty   = reduce-scatter(sum_g p_g)        rank g receives its cnt columns
-//   x, w  = x-phase epilogue on the slice    (EpiXIter over the slice)
-//   w     = all-gather(w slices)             every rank needs all of w
+//   aty   = reduce-scatter(sum_g p_g)        rank g receives its owned columns
+//   x, w  = x-phase epilogue on owned cols   (EpiXIter)
+//   w     = all-gather(w)                    every rank needs all of w
 //   y_g   = y-phase on A_g w                 local SELL kernel (EpiYIter)
 // i.e. the north star's all-reduce of the A^T y partials, split as RS + AG so
-// the n-length elementwise work is done once, not P times.  Checkpoint sums
-// (KKT, merit, sigma) are per-rank fixed-order partials, then all-gathered and
-// summed in rank order, so every rank makes the same host decisions.
+// the n-length elementwise work is done once, not P times.  With NCCL and K > 1
+// the four steps run chunk by chunk: chunk q's reduce-scatter, epilogue and
+// all-gather (on a second stream) overlap the partial SpMV of chunk q+1.
+// Checkpoint sums (KKT, merit, sigma) are per-rank fixed-order partials, then
+// all-gathered and summed in rank order, so every rank makes the same host
+// decisions.
 //
 // Two transports behind one interface:
 //   * NCCL (one rank per process, one GPU each; ncclReduceScatter /
@@ -52,49 +56,75 @@ struct EpiStore {
   __device__ void finish(int j, double s, double *) { out[j] = s; }
 };
 
-// column epilogue over a slice: epi.finish(j, s[j - j0]) for j in [j0, j1)
+// Column ownership: the padded column range is K chunks of CW = P*cw columns;
+// rank g owns columns i*CW + g*cw + [0, cw) of every chunk i.  Owned entries
+// are enumerated idx = i*cw + t; the reduce-scattered partials of rank g are
+// stored in that order (xslice[idx]).  K = 1 is one contiguous slice per rank.
+__device__ __forceinline__ long long owned_col(int idx, int gr, int cw, int CW) {
+  const int i = idx / cw;
+  return (long long)i * CW + (long long)gr * cw + (idx - i * cw);
+}
+
+// column epilogue over the owned columns of chunks [i0, i1): epi.finish(j, s[idx])
 template <class Epi>
 __global__ void __launch_bounds__(kThreads)
-k_cols(int j0, int j1, const double *__restrict__ s, Epi epi, double *part) {
+k_cols(int gr, int cw, int CW, int i0, int i1, int n, const double *__restrict__ s, Epi epi,
+       double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll
   for (int q = 0; q < (Epi::NQ > 0 ? Epi::NQ : 1); ++q) acc[q] = 0.0;
   if (!epi.enter()) return;
-  for (int j = j0 + blockIdx.x * kThreads + threadIdx.x; j < j1; j += gridDim.x * kThreads) {
-    epi.prefetch(j);
-    epi.finish(j, s[j - j0], acc);
+  for (int idx = i0 * cw + blockIdx.x * kThreads + threadIdx.x; idx < i1 * cw;
+       idx += gridDim.x * kThreads) {
+    const long long j = owned_col(idx, gr, cw, CW);
+    if (j < n) {
+      epi.prefetch((int)j);
+      epi.finish((int)j, s[idx], acc);
+    }
   }
   if constexpr (Epi::NQ > 0) block_reduce_store<Epi::NQ>(acc, part, gridDim.x);
 }
 
-// power-method u^2 over a slice (sparse.py:178 check), one partial per CTA
-__global__ void __launch_bounds__(kThreads) k_slice_sumsq(const double *s, int cnt, double *part) {
+// sum of squares over the owned entries (owned columns of a, or a compact slice)
+__global__ void __launch_bounds__(kThreads)
+k_owned_sumsq(const double *a, int compact, int gr, int cw, int CW, int cnt, int n, double *part) {
   double acc[1] = {0.0};
-  for (int j = blockIdx.x * kThreads + threadIdx.x; j < cnt; j += gridDim.x * kThreads)
-    acc[0] = __dadd_rn(acc[0], sq(s[j]));
+  for (int idx = blockIdx.x * kThreads + threadIdx.x; idx < cnt; idx += gridDim.x * kThreads) {
+    const long long j = owned_col(idx, gr, cw, CW);
+    if (j < n) acc[0] = __dadd_rn(acc[0], sq(compact ? a[idx] : a[j]));
+  }
   block_reduce_store<1>(acc, part, gridDim.x);
 }
 
+// owned entries of a compact slice into their positions of a full vector
+__global__ void k_owned_scatter(const double *slice, double *vec, int gr, int cw, int CW, int cnt) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt; idx += gridDim.x * blockDim.x)
+    vec[owned_col(idx, gr, cw, CW)] = slice[idx];
+}
+
 // ---- local transport: all ranks' buffers on one device ----------------------
-// out_g[j] = sum_{r = 0..P-1} part_r[g*cnt + j]   (rank order)
-__global__ void k_rs_local(PtrSet part, PtrSet out, int P, int cnt) {
-  const long long total = (long long)P * cnt;
+// out_g[i*cw + t] = sum_{r = 0..P-1} part_r[i*CW + g*cw + t]   (rank order)
+__global__ void k_rs_local(PtrSet part, PtrSet out, int P, int K, int cw, int CW) {
+  const long long per = (long long)K * cw, total = (long long)P * per;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(e / per), idx = (int)(e % per);
+    const long long pos = owned_col(idx, g, cw, CW);
     double s = 0.0;
-    for (int r = 0; r < P; ++r) s = __dadd_rn(s, part.p[r][e]);
-    out.p[e / cnt][e % cnt] = s;
+    for (int r = 0; r < P; ++r) s = __dadd_rn(s, part.p[r][pos]);
+    out.p[g][idx] = s;
   }
 }
-// all-gather: vec_r[g*cnt + j] = src_g[j] for every r (src may alias vec_g + g*cnt)
-__global__ void k_ag_local(PtrSet src, PtrSet vec, int P, int cnt) {
-  const long long total = (long long)P * cnt;
+// in-place all-gather: every rank's owned entries copied to the other ranks
+__global__ void k_ag_local(PtrSet vec, int P, int K, int cw, int CW) {
+  const long long per = (long long)K * cw, total = (long long)P * per;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(e / cnt);
-    const double v = src.p[g][e % cnt];
+    const int g = (int)(e / per), idx = (int)(e % per);
+    const long long pos = owned_col(idx, g, cw, CW);
+    const double v = vec.p[g][pos];
     for (int r = 0; r < P; ++r)
-      if (vec.p[r] + e != src.p[g] + e % cnt) vec.p[r][e] = v;
+      if (r != g) vec.p[r][pos] = v;
   }
 }
 // all-reduce in place over n entries (op 0 = sum in rank order, 2 = max)
@@ -185,19 +215,29 @@ NcclApi &nccl() {
 // per-rank buffers of the row-block mode (carved from the caller's rb workspace)
 struct RbRank {
   hpr_ctx *c = nullptr;
-  double *xpart = nullptr;   // n_pad: partial A_g^T v
-  double *xslice = nullptr;  // cnt: reduced slice
+  double *xpart = nullptr;   // npad: partial A_g^T v (entries >= n stay 0)
+  double *xslice = nullptr;  // K * cw: reduce-scattered owned entries
   double *gath = nullptr;    // P * 64: all-gathered scalars (NCCL transport)
   int64_t row0 = 0;          // first global row
 };
 
-size_t rb_layout(int64_t n, int P, size_t *o_xpart, size_t *o_xslice, size_t *o_gath) {
-  const int64_t cnt = (n + P - 1) / P;
+// chunk geometry: K chunks of P slices of cw columns (cw a multiple of the SELL
+// window when K > 1, so a chunk is a whole number of SELL windows of A^T)
+void rb_dims(int64_t n, int P, int K, int64_t *cw, int64_t *npad) {
+  int64_t w = (n + (int64_t)K * P - 1) / ((int64_t)K * P);
+  if (K > 1) w = (w + kWindow - 1) / kWindow * kWindow;
+  *cw = std::max<int64_t>(w, 1);
+  *npad = *cw * P * K;
+}
+
+size_t rb_layout(int64_t n, int P, int K, size_t *o_xpart, size_t *o_xslice, size_t *o_gath) {
+  int64_t cw, npad;
+  rb_dims(n, P, K, &cw, &npad);
   size_t off = 0;
   *o_xpart = off;
-  off = align_up(off + sizeof(double) * cnt * P, 256);
+  off = align_up(off + sizeof(double) * npad, 256);
   *o_xslice = off;
-  off = align_up(off + sizeof(double) * std::max<int64_t>(cnt, 1), 256);
+  off = align_up(off + sizeof(double) * cw * K, 256);
   *o_gath = off;
   off = align_up(off + sizeof(double) * 64 * P, 256);
   return off;
@@ -209,17 +249,22 @@ struct hpr_group {
   int P = 1;          // ranks in the group
   int rank0 = 0;      // global rank of local rank 0
   int nlocal = 1;
-  int64_t n = 0, cnt = 0;
+  int64_t n = 0;
+  int K = 1;                       // column chunks (overlap granularity)
+  int64_t cw = 0, CW = 0, npad = 0;
   std::vector<RbRank> r;
   ncclComm_t comm = nullptr;
   bool use_nccl = false;
   cudaStream_t stream = nullptr;   // ctx[0]'s stream (local transport: shared)
+  cudaStream_t comm_stream = nullptr;          // NCCL + chunk epilogues, K > 1
+  std::vector<cudaEvent_t> ev_chunk;           // per chunk: partial SpMV done
+  cudaEvent_t ev_comm = nullptr;               // comm stream joined back
   std::map<int, cudaGraphExec_t> inner_graphs;
   cudaGraphExec_t pow_graph = nullptr;
   bool inner_timed = false, ckpt_timed = false;
 
-  int j0(int l) const { return (int)std::min<int64_t>((int64_t)(rank0 + l) * cnt, n); }
-  int j1(int l) const { return (int)std::min<int64_t>((int64_t)(rank0 + l + 1) * cnt, n); }
+  int gr(int l) const { return rank0 + l; }    // global rank of local rank l
+  int owned() const { return (int)(K * cw); }
 };
 
 namespace {
@@ -230,47 +275,47 @@ PtrSet ptrs(hpr_group *g, double *RbRank::*f) {
   return s;
 }
 
-// sum of xpart over ranks -> xslice of each rank
-int g_reduce_scatter(hpr_group *g) {
-  if (g->P == 1 && !g->use_nccl) {
-    CK(cudaMemcpyAsync(g->r[0].xslice, g->r[0].xpart, sizeof(double) * g->cnt,
-                       cudaMemcpyDeviceToDevice, g->stream));
-    return HPR_OK;
-  }
+// sum of xpart over ranks -> xslice (owned entries) of each rank, chunks [i0, i1)
+int g_reduce_scatter(hpr_group *g, cudaStream_t st = nullptr, int i0 = 0, int i1 = -1) {
+  if (!st) st = g->stream;
+  if (i1 < 0) i1 = g->K;
   if (g->use_nccl) {
-    NK(nccl().reduceScatter(g->r[0].xpart, g->r[0].xslice, (size_t)g->cnt, ncclFloat64, ncclSum,
-                            g->comm, g->r[0].c->stream));
+    for (int i = i0; i < i1; ++i)
+      NK(nccl().reduceScatter(g->r[0].xpart + (size_t)i * g->CW, g->r[0].xslice + (size_t)i * g->cw,
+                              (size_t)g->cw, ncclFloat64, ncclSum, g->comm, st));
     return HPR_OK;
   }
-  const long long total = (long long)g->P * g->cnt;
-  k_rs_local<<<grid_for(total), 256, 0, g->stream>>>(ptrs(g, &RbRank::xpart), ptrs(g, &RbRank::xslice),
-                                                     g->P, (int)g->cnt);
+  if (g->P == 1) {
+    CK(cudaMemcpyAsync(g->r[0].xslice, g->r[0].xpart, sizeof(double) * g->cw * g->K,
+                       cudaMemcpyDeviceToDevice, st));
+    return HPR_OK;
+  }
+  const long long total = (long long)g->P * g->owned();
+  k_rs_local<<<grid_for(total), 256, 0, st>>>(ptrs(g, &RbRank::xpart), ptrs(g, &RbRank::xslice),
+                                              g->P, g->K, (int)g->cw, (int)g->CW);
   CKL();
   g->r[0].c->launches += 1;
   return HPR_OK;
 }
 
-// every rank's full vector vec(l) <- concatenation of the ranks' slices.  src(l)
-// is the slice owned by local rank l (may alias vec(l) + j0(l)).
-template <class VecOf, class SrcOf>
-int g_all_gather(hpr_group *g, VecOf vec, SrcOf src) {
-  if (g->P == 1 && !g->use_nccl) {
-    const double *s = src(0);
-    double *v = vec(0);
-    if (s != v) CK(cudaMemcpyAsync(v, s, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, g->stream));
-    return HPR_OK;
-  }
+// in-place all-gather: every rank's full vector vec(l) receives the other
+// ranks' owned entries (chunks [i0, i1))
+template <class VecOf>
+int g_all_gather(hpr_group *g, VecOf vec, cudaStream_t st = nullptr, int i0 = 0, int i1 = -1) {
+  if (!st) st = g->stream;
+  if (i1 < 0) i1 = g->K;
   if (g->use_nccl) {
-    NK(nccl().allGather(src(0), vec(0), (size_t)g->cnt, ncclFloat64, g->comm, g->r[0].c->stream));
+    double *v = vec(0);
+    for (int i = i0; i < i1; ++i)
+      NK(nccl().allGather(v + (size_t)i * g->CW + (size_t)g->gr(0) * g->cw, v + (size_t)i * g->CW,
+                          (size_t)g->cw, ncclFloat64, g->comm, st));
     return HPR_OK;
   }
-  PtrSet ps{}, pv{};
-  for (int l = 0; l < g->nlocal; ++l) {
-    ps.p[l] = const_cast<double *>(src(l));
-    pv.p[l] = vec(l);
-  }
-  const long long total = (long long)g->P * g->cnt;
-  k_ag_local<<<grid_for(total), 256, 0, g->stream>>>(ps, pv, g->P, (int)g->cnt);
+  if (g->P == 1) return HPR_OK;
+  PtrSet pv{};
+  for (int l = 0; l < g->nlocal; ++l) pv.p[l] = vec(l);
+  const long long total = (long long)g->P * g->owned();
+  k_ag_local<<<grid_for(total), 256, 0, st>>>(pv, g->P, g->K, (int)g->cw, (int)g->CW);
   CKL();
   g->r[0].c->launches += 1;
   return HPR_OK;
@@ -326,12 +371,33 @@ int g_at_partial(hpr_group *g, int l, bool scaled, const double *v, const PowSta
   return launch_sell(c, c->mat_at(scaled), v, es, nullptr, nullptr);
 }
 
-template <class Epi>
-int g_cols(hpr_group *g, int l, const Epi &epi, double *part, int *grid_out) {
+// the partial of one column chunk: rows [q*CW, (q+1)*CW) of A_l^T (whole SELL
+// windows); the long rows ride with chunk 0 so they precede every reduction
+int g_at_partial_chunk(hpr_group *g, int l, const double *v, int q) {
   hpr_ctx *c = g->r[l].c;
-  const int j0 = g->j0(l), j1 = g->j1(l);
-  const int grid = std::max(1, std::min(grid_for(std::max(j1 - j0, 1), kThreads), c->num_sms * 4));
-  k_cols<Epi><<<grid, kThreads, 0, c->stream>>>(j0, j1, g->r[l].xslice, epi, part);
+  SellMat M = c->mat_at(true);
+  const long long s0 = (long long)q * g->CW / kSlice;
+  M.slice_ptr += s0;
+  M.slice_row += s0 * kSlice;
+  M.slice_len += s0 * kSlice;
+  M.nslices = (int)std::max<long long>(0, std::min<long long>(g->CW / kSlice, M.nslices - s0));
+  if (q > 0) M.nlong = 0;
+  EpiStore es{};
+  es.out = g->r[l].xpart;
+  es.S = nullptr;
+  return launch_sell(c, M, v, es, nullptr, nullptr);
+}
+
+template <class Epi>
+int g_cols(hpr_group *g, int l, const Epi &epi, double *part, int *grid_out,
+           cudaStream_t st = nullptr, int i0 = 0, int i1 = -1) {
+  hpr_ctx *c = g->r[l].c;
+  if (!st) st = c->stream;
+  if (i1 < 0) i1 = g->K;
+  const int cnt = (i1 - i0) * (int)g->cw;
+  const int grid = std::max(1, std::min(grid_for(std::max(cnt, 1), kThreads), c->num_sms * 4));
+  k_cols<Epi><<<grid, kThreads, 0, st>>>(g->gr(l), (int)g->cw, (int)g->CW, i0, i1, (int)g->n,
+                                         g->r[l].xslice, epi, part);
   CKL();
   c->launches += 1;
   if (grid_out) *grid_out = grid;
@@ -447,17 +513,19 @@ int hpr_nccl_unique_id(void *id, size_t bytes) {
   return HPR_OK;
 }
 
-int hpr_group_ws_bytes(int64_t n, int nranks, size_t *bytes) {
-  if (!bytes || n < 1 || nranks < 1) return fail(HPR_EINVAL, "bad argument");
+int hpr_group_dims(int64_t n, int nranks, int chunks, int64_t *npad, size_t *ws_bytes) {
+  if (!npad || !ws_bytes || n < 1 || nranks < 1 || chunks < 1) return fail(HPR_EINVAL, "bad argument");
+  int64_t cw;
+  rb_dims(n, nranks, chunks, &cw, npad);
   size_t a, b, c;
-  *bytes = rb_layout(n, nranks, &a, &b, &c);
+  *ws_bytes = rb_layout(n, nranks, chunks, &a, &b, &c);
   return HPR_OK;
 }
 
 int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *const *rb_ws,
-                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0,
+                     const int64_t *row0, size_t rb_ws_bytes, int nranks, int rank0, int chunks,
                      const void *nccl_id, size_t id_bytes) {
-  if (!out || !ctxs || !rb_ws || !row0 || nlocal < 1 || nranks < 1)
+  if (!out || !ctxs || !rb_ws || !row0 || nlocal < 1 || nranks < 1 || chunks < 1)
     return fail(HPR_EINVAL, "bad argument");
   if (nlocal > kMaxLocal) return fail(HPR_EINVAL, "too many local ranks");
   const bool use_nccl = nccl_id != nullptr;
@@ -466,7 +534,7 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
     return fail(HPR_EINVAL, "local transport: all ranks must be local");
   const int64_t n = ctxs[0]->d.n;
   size_t o_xpart, o_xslice, o_gath;
-  const size_t need = rb_layout(n, nranks, &o_xpart, &o_xslice, &o_gath);
+  const size_t need = rb_layout(n, nranks, chunks, &o_xpart, &o_xslice, &o_gath);
   if (rb_ws_bytes < need) return fail(HPR_EINVAL, "row-block workspace too small");
   for (int l = 0; l < nlocal; ++l) {
     if (!ctxs[l] || !rb_ws[l]) return fail(HPR_EINVAL, "null context or workspace");
@@ -479,7 +547,9 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
   g->rank0 = rank0;
   g->nlocal = nlocal;
   g->n = n;
-  g->cnt = (n + nranks - 1) / nranks;
+  g->K = chunks;
+  rb_dims(n, nranks, chunks, &g->cw, &g->npad);
+  g->CW = g->cw * nranks;
   g->stream = ctxs[0]->stream;
   g->use_nccl = use_nccl;
   for (int l = 0; l < nlocal; ++l) {
@@ -491,6 +561,15 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
     rr.gath = (double *)(w + o_gath);
     rr.row0 = row0[l];
     g->r.push_back(rr);
+    // the partial's padding rows (n .. npad) are never written: keep them 0
+    cudaMemsetAsync(rr.xpart, 0, sizeof(double) * g->npad, g->stream);
+  }
+  if (use_nccl && chunks > 1) {
+    cudaSetDevice(ctxs[0]->device);
+    cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking);
+    g->ev_chunk.resize(chunks);
+    for (auto &e : g->ev_chunk) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming);
   }
   if (g->use_nccl) {
     if (!nccl().ok) {
@@ -519,14 +598,18 @@ int hpr_group_destroy(hpr_group *g) {
   for (auto &kv : g->inner_graphs) cudaGraphExecDestroy(kv.second);
   if (g->pow_graph) cudaGraphExecDestroy(g->pow_graph);
   if (g->comm) nccl().commDestroy(g->comm);
+  for (auto &e : g->ev_chunk) cudaEventDestroy(e);
+  if (g->ev_comm) cudaEventDestroy(g->ev_comm);
+  if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
   delete g;
   return HPR_OK;
 }
 
-int hpr_group_col_range(hpr_group *g, int local, int64_t *j0, int64_t *j1) {
-  if (!g || !j0 || !j1 || local < 0 || local >= g->nlocal) return fail(HPR_EINVAL, "bad argument");
-  *j0 = g->j0(local);
-  *j1 = g->j1(local);
+int hpr_group_col_layout(hpr_group *g, int64_t *chunks, int64_t *cw, int64_t *npad) {
+  if (!g || !chunks || !cw || !npad) return fail(HPR_EINVAL, "bad argument");
+  *chunks = g->K;
+  *cw = g->cw;
+  *npad = g->npad;
   return HPR_OK;
 }
 
@@ -605,11 +688,11 @@ int hpr_group_scale(hpr_group *g, int ruiz_iters, int pock_chambolle, int bc_nor
       const hpr_buffers &B = c->B;
       Parts P = parts_of(c);
       const int m = (int)c->d.m;
-      const int j0 = g->j0(l), cntl = g->j1(l) - j0;
-      const int nb0 = sumsq_blocks(m), nb1 = sumsq_blocks(std::max(cntl, 1));
+      const int nb0 = sumsq_blocks(m), nb1 = sumsq_blocks(g->owned());
       double *pb = P.misc + (2 * bank) * kSumsqBlocks, *pc = P.misc + (2 * bank + 1) * kSumsqBlocks;
       k_sumsq<<<nb0, kThreads, 0, c->stream>>>(orig ? B.b : B.b_s, m, pb);
-      k_sumsq<<<nb1, kThreads, 0, c->stream>>>((orig ? B.c : B.c_s) + j0, cntl, pc);
+      k_owned_sumsq<<<nb1, kThreads, 0, c->stream>>>(orig ? B.c : B.c_s, 0, g->gr(l), (int)g->cw,
+                                                     (int)g->CW, g->owned(), n, pc);
       CKL();
       c->launches += 2;
       segs[l].push_back({pb, nb0, slot_b});
@@ -732,9 +815,9 @@ int hpr_group_power(hpr_group *g, double tol, int max_iters, hpr_power_out *out)
     for (int l = 0; l < g->nlocal; ++l) {
       hpr_ctx *c = g->r[l].c;
       Parts P = parts_of(c);
-      const int cntl = g->j1(l) - g->j0(l);
-      const int nb = sumsq_blocks(std::max(cntl, 1));
-      k_slice_sumsq<<<nb, kThreads, 0, c->stream>>>(g->r[l].xslice, cntl, P.powt);
+      const int nb = sumsq_blocks(g->owned());
+      k_owned_sumsq<<<nb, kThreads, 0, c->stream>>>(g->r[l].xslice, 1, g->gr(l), (int)g->cw,
+                                                    (int)g->CW, g->owned(), (int)g->n, P.powt);
       CKL();
       c->launches += 1;
       segs[l].push_back({P.powt, nb, R_POW_U2});
@@ -775,8 +858,13 @@ int hpr_group_power(hpr_group *g, double tol, int max_iters, hpr_power_out *out)
       // u = A^T v: partial -> reduce-scatter -> all-gather
       for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, vbuf(l), g->r[l].c->pow);
       if (!rc) rc = g_reduce_scatter(g);
-      if (!rc)
-        rc = g_all_gather(g, ubuf, [&](int l) -> const double * { return g->r[l].xslice; });
+      for (int l = 0; l < g->nlocal && !rc; ++l) {
+        hpr_ctx *c = g->r[l].c;
+        k_owned_scatter<<<grid_for(g->owned()), 256, 0, c->stream>>>(
+            g->r[l].xslice, ubuf(l), g->gr(l), (int)g->cw, (int)g->CW, g->owned());
+        c->launches += 1;
+      }
+      if (!rc) rc = g_all_gather(g, ubuf);
       // w = A_g u, local sums v.w and w.w
       for (int l = 0; l < g->nlocal && !rc; ++l) {
         hpr_ctx *c = g->r[l].c;
@@ -850,25 +938,44 @@ int hpr_group_run_inner(hpr_group *g, int steps, int64_t t, int64_t k, double si
     cudaGraph_t gr;
     CK(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
     auto wvec = [&](int l) { return g->r[l].c->B.w; };
-    auto wsl = [&](int l) -> const double * { return g->r[l].c->B.w + g->j0(l); };
+    auto xepi = [&](int l, int i) {
+      const hpr_buffers &B = g->r[l].c->B;
+      EpiXIter ex{};
+      ex.c = B.c_s;
+      ex.lo = B.lower_s;
+      ex.up = B.upper_s;
+      ex.anc = B.anc_x;
+      ex.x = B.x;
+      ex.w = B.w;
+      ex.P = g->r[l].c->params;
+      ex.step = i;
+      return ex;
+    };
+    const bool overlap = g->use_nccl && g->K > 1 && g->comm_stream;
     for (int i = 0; i < steps && !rc; ++i) {
-      for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, g->r[l].c->B.y, nullptr);
-      if (!rc) rc = g_reduce_scatter(g);
-      for (int l = 0; l < g->nlocal && !rc; ++l) {
-        hpr_ctx *c = g->r[l].c;
-        const hpr_buffers &B = c->B;
-        EpiXIter ex{};
-        ex.c = B.c_s;
-        ex.lo = B.lower_s;
-        ex.up = B.upper_s;
-        ex.anc = B.anc_x;
-        ex.x = B.x;
-        ex.w = B.w;
-        ex.P = c->params;
-        ex.step = i;
-        rc = g_cols(g, l, ex, nullptr, nullptr);
+      if (overlap) {
+        // chunk by chunk: the partial A_g^T y of chunk q is reduce-scattered,
+        // finished (x-phase epilogue) and all-gathered on the comm stream while
+        // the partial of chunk q+1 is computed on the main stream
+        hpr_ctx *c = g->r[0].c;
+        for (int q = 0; q < g->K && !rc; ++q) {
+          rc = g_at_partial_chunk(g, 0, c->B.y, q);
+          if (rc) break;
+          CK(cudaEventRecord(g->ev_chunk[q], c->stream));
+          CK(cudaStreamWaitEvent(g->comm_stream, g->ev_chunk[q], 0));
+          rc = g_reduce_scatter(g, g->comm_stream, q, q + 1);
+          if (!rc) rc = g_cols(g, 0, xepi(0, i), nullptr, nullptr, g->comm_stream, q, q + 1);
+          if (!rc) rc = g_all_gather(g, wvec, g->comm_stream, q, q + 1);
+        }
+        if (rc) break;
+        CK(cudaEventRecord(g->ev_comm, g->comm_stream));
+        CK(cudaStreamWaitEvent(c->stream, g->ev_comm, 0));
+      } else {
+        for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_at_partial(g, l, true, g->r[l].c->B.y, nullptr);
+        if (!rc) rc = g_reduce_scatter(g);
+        for (int l = 0; l < g->nlocal && !rc; ++l) rc = g_cols(g, l, xepi(l, i), nullptr, nullptr);
+        if (!rc) rc = g_all_gather(g, wvec);
       }
-      if (!rc) rc = g_all_gather(g, wvec, wsl);
       for (int l = 0; l < g->nlocal && !rc; ++l) {
         hpr_ctx *c = g->r[l].c;
         const hpr_buffers &B = c->B;
@@ -950,11 +1057,8 @@ int hpr_group_checkpoint(hpr_group *g, double sigma, double lamsig, int term_ori
   }
   if (rc) return rc;
   // the y phase and the row KKT terms gather wtmp and cand_x over all columns
-  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.wtmp; },
-                    [&](int l) -> const double * { return g->r[l].c->B.wtmp + g->j0(l); });
-  if (!rc)
-    rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[slot]; },
-                      [&](int l) -> const double * { return g->r[l].c->B.cand_x[slot] + g->j0(l); });
+  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.wtmp; });
+  if (!rc) rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[slot]; });
   for (int l = 0; l < g->nlocal && !rc; ++l) {
     hpr_ctx *c = g->r[l].c;
     const hpr_buffers &B = c->B;
@@ -1056,11 +1160,8 @@ int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *
     }
   }
   // x and z are valid on each rank's slice only: gather them
-  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[fs]; },
-                    [&](int l) -> const double * { return g->r[l].c->B.cand_x[fs] + g->j0(l); });
-  if (!rc)
-    rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_z[fs]; },
-                      [&](int l) -> const double * { return g->r[l].c->B.cand_z[fs] + g->j0(l); });
+  rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_x[fs]; });
+  if (!rc) rc = g_all_gather(g, [&](int l) { return g->r[l].c->B.cand_z[fs]; });
   if (rc) return rc;
   return g_kkt_common(g, 1, fs, out);
 }

@@ -30,6 +30,25 @@ from .problem import stacked_arrays
 NCCL_ID_BYTES = 128
 
 
+def default_chunks(nranks: int, nccl: bool) -> int:
+    """Column chunks of the inner loop: with NCCL over several GPUs the chunk
+    q collectives overlap the partial SpMV of chunk q+1 (HPR_RB_CHUNKS
+    overrides)."""
+    import os
+    env = os.environ.get("HPR_RB_CHUNKS")
+    if env:
+        return max(1, int(env))
+    return 4 if (nccl and nranks > 1) else 1
+
+
+def group_dims(n: int, nranks: int, chunks: int):
+    """(npad, row-block workspace bytes) of the native group."""
+    npad, ws = ctypes.c_int64(0), ctypes.c_size_t(0)
+    N.call("hpr_group_dims", ctypes.c_int64(n), int(nranks), int(chunks), ctypes.byref(npad),
+           ctypes.byref(ws))
+    return int(npad.value), int(ws.value)
+
+
 def partition_rows(row_offsets, parts: int) -> np.ndarray:
     """Boundaries r_0 = 0 < ... < r_P = m of P contiguous row blocks with
     nonzeros as even as whole rows allow (block g = rows [r_g, r_{g+1})).
@@ -63,7 +82,7 @@ def block_arrays(ro, ci, v, rhs, m1, r0, r1):
 class RowBlockGroup:
     """P row blocks + one native group (DeviceLP-compatible surface)."""
 
-    def __init__(self, blocks, row0, n, m_total, m1_total, nnz_total, nranks, rank0,
+    def __init__(self, blocks, row0, n, m_total, m1_total, nnz_total, nranks, rank0, chunks,
                  nccl_id=None):
         self.blocks = blocks                   # list[DeviceLP], local ranks
         self.row0 = list(row0)
@@ -76,13 +95,11 @@ class RowBlockGroup:
         self.analyzed = False
         self.nccl = nccl_id is not None
         torch = _torch()
-        sz = ctypes.c_size_t(0)
-        N.call("hpr_group_ws_bytes", ctypes.c_int64(self.n), self.P, ctypes.byref(sz))
+        self.chunks = int(chunks)
+        self.npad, sz = group_dims(self.n, self.P, self.chunks)
         with torch.cuda.stream(self.stream):
-            self.rb_ws = [torch.empty(int(sz.value), dtype=torch.uint8, device=b.device)
-                          for b in blocks]
-        self._blocks_analyzed = False
-        self._sz = int(sz.value)
+            self.rb_ws = [torch.empty(sz, dtype=torch.uint8, device=b.device) for b in blocks]
+        self._sz = sz
         self._nccl_id = nccl_id
         self.g = None
 
@@ -95,7 +112,8 @@ class RowBlockGroup:
         rhs = np.concatenate([np.asarray(problem.b_eq, np.float64),
                               np.asarray(problem.b_ineq, np.float64)])
         bounds = partition_rows(ro, parts)
-        n_pad = -(-n // parts) * parts
+        chunks = default_chunks(parts, False)
+        n_pad, _ = group_dims(n, parts, chunks)
         if stream is None:
             stream = torch.cuda.Stream(device=torch.device("cuda", device))
         blocks = []
@@ -104,7 +122,7 @@ class RowBlockGroup:
             blocks.append(DeviceLP.from_arrays(bro, bci, bv, int(bounds[g + 1] - bounds[g]), n,
                                                bm1, bb, problem.c, problem.lower, problem.upper,
                                                device=device, stream=stream, n_alloc=n_pad))
-        return cls(blocks, bounds[:-1], n, m, m1, int(ro[-1]), parts, 0)
+        return cls(blocks, bounds[:-1], n, m, m1, int(ro[-1]), parts, 0, chunks)
 
     @classmethod
     def distributed(cls, block, *, n, m_total, m1_total, nnz_total, row0, rank, world,
@@ -112,10 +130,12 @@ class RowBlockGroup:
         """This process's rank: ``block`` = (row_offsets, col_indices, values, m1_local,
         b, c, lower, upper) of its rows; ``nccl_id`` = 128 bytes from rank 0."""
         ro, ci, v, m1_local, b, c, lo, up = block
-        n_pad = -(-n // world) * world
+        chunks = default_chunks(world, True)
+        n_pad, _ = group_dims(n, world, chunks)
         dev = DeviceLP.from_arrays(ro, ci, v, len(ro) - 1, n, m1_local, b, c, lo, up,
                                    device=device, n_alloc=n_pad)
-        return cls([dev], [row0], n, m_total, m1_total, nnz_total, world, rank, nccl_id=nccl_id)
+        return cls([dev], [row0], n, m_total, m1_total, nnz_total, world, rank, chunks,
+                   nccl_id=nccl_id)
 
     def _create(self):
         nl = len(self.blocks)
@@ -126,11 +146,12 @@ class RowBlockGroup:
         if self._nccl_id is not None:
             idb = ctypes.create_string_buffer(bytes(self._nccl_id), NCCL_ID_BYTES)
             N.call("hpr_group_create", ctypes.byref(g), nl, ctxs, wss, r0,
-                   ctypes.c_size_t(self._sz), self.P, self.rank0, idb,
+                   ctypes.c_size_t(self._sz), self.P, self.rank0, self.chunks, idb,
                    ctypes.c_size_t(NCCL_ID_BYTES))
         else:
             N.call("hpr_group_create", ctypes.byref(g), nl, ctxs, wss, r0,
-                   ctypes.c_size_t(self._sz), self.P, self.rank0, None, ctypes.c_size_t(0))
+                   ctypes.c_size_t(self._sz), self.P, self.rank0, self.chunks, None,
+                   ctypes.c_size_t(0))
         self.g = g
 
     # -- DeviceLP surface used by driver.solve --------------------------------
@@ -205,10 +226,15 @@ class RowBlockGroup:
     def synchronize(self):
         self.stream.synchronize()
 
-    def col_range(self, local: int = 0):
-        j0, j1 = ctypes.c_int64(0), ctypes.c_int64(0)
-        N.call("hpr_group_col_range", self.g, int(local), ctypes.byref(j0), ctypes.byref(j1))
-        return int(j0.value), int(j1.value)
+    def owned_columns(self, local: int = 0) -> np.ndarray:
+        """Column indices owned by local rank ``local`` (hpr_group_col_layout)."""
+        k, cw, npad = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        N.call("hpr_group_col_layout", self.g, ctypes.byref(k), ctypes.byref(cw),
+               ctypes.byref(npad))
+        k, cw = int(k.value), int(cw.value)
+        g = self.rank0 + local
+        cols = (np.arange(k)[:, None] * (self.P * cw) + g * cw + np.arange(cw)[None, :]).ravel()
+        return cols[cols < self.n]
 
     def to_host(self, name, slot=None):
         """Row vectors: the ranks' blocks concatenated (all-gathered over
@@ -225,14 +251,17 @@ class RowBlockGroup:
             return np.concatenate(parts)
         pieces = []
         for l, b in enumerate(self.blocks):
-            j0, j1 = self.col_range(l)
-            pieces.append(b.to_host(name, slot)[j0:j1])
+            cols = self.owned_columns(l)
+            pieces.append((cols, b.to_host(name, slot)[cols]))
         if self.nccl and self.P > 1:
             import torch.distributed as dist
             got = [None] * self.P
             dist.all_gather_object(got, pieces[0])
             pieces = got
-        return np.concatenate(pieces)
+        out = np.empty(self.n)
+        for cols, vals in pieces:
+            out[cols] = vals
+        return out
 
     def close(self):
         if self.g is not None and self.g.value:

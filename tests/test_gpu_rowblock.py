@@ -32,8 +32,9 @@ def _traj_rel(y, x, ry, rx):
         np.sum(ry ** 2) + np.sum(rx ** 2))
 
 
-@pytest.mark.parametrize("parts", [1, 2, 3, 5])
-def test_partitioned_trajectory_c1(parts):
+@pytest.mark.parametrize("parts,chunks", [(1, 1), (2, 1), (3, 1), (5, 1), (2, 3), (4, 2)])
+def test_partitioned_trajectory_c1(parts, chunks, monkeypatch):
+    monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
     d = np.load(f"{GOLDEN}/c1_golden.npz")
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     grp = RowBlockGroup.local(prob, parts)
@@ -93,8 +94,9 @@ def test_partitioned_scaling_and_power(parts):
     grp.close()
 
 
-@pytest.mark.parametrize("parts", [2, 4])
-def test_partitioned_solve_c1_vs_reference(golden_reports, parts):
+@pytest.mark.parametrize("parts,chunks", [(2, 1), (4, 1), (3, 2)])
+def test_partitioned_solve_c1_vs_reference(golden_reports, parts, chunks, monkeypatch):
+    monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     for key in ("c1", "c1_1e-8"):
         g = golden_reports[key]
@@ -131,7 +133,12 @@ def _free_port():
     return p
 
 
-def test_nccl_transport_world1(golden_reports):
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_nccl_transport_world1(golden_reports, chunks, monkeypatch):
+    """chunks > 1 runs the overlapped pipeline (comm stream, per-chunk events,
+    chunked NCCL reduce-scatter / all-gather) -- with one rank the collectives
+    are copies, but the captured multi-stream graph is the P-GPU one."""
+    monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
     import torch
     import torch.distributed as dist
     from paper_2408_12179_b200 import _native as N
