@@ -188,10 +188,13 @@ class DeviceLP:
         with _Staging.lock:
             stage = _Staging.get(total)
             host = stage.numpy()
+            # each array's DMA is issued as soon as it is staged, so the copy of
+            # array i overlaps the host-side fill of array i+1
             for (name, dt, ln, fill), o in zip(spec, offs):
-                fill(host[o:o + ln * np.dtype(dt).itemsize].view(dt))
-            with torch.cuda.stream(self.stream):
-                self._inputs.copy_(stage[:total], non_blocking=True)
+                nb = ln * np.dtype(dt).itemsize
+                fill(host[o:o + nb].view(dt))
+                with torch.cuda.stream(self.stream):
+                    self._inputs[o:o + nb].copy_(stage[o:o + nb], non_blocking=True)
             self.stream.synchronize()       # the staging buffer is reusable after this
         if getattr(self, "ctx", None) is not None:
             self.h2d_bytes = total
