@@ -299,3 +299,28 @@ def test_mps_round_trip_solve_bit_for_bit():
     assert a.iterations == b.iterations
     assert a.primal_objective == b.primal_objective
     assert np.array_equal(a.solution.x, b.solution.x)
+
+
+def test_flow_lp_downscaled_vs_oracle():
+    """C3's generator down-scaled: bit-exact iterations and a
+    full solve with the reference's status / iteration count / restart
+    triggers and objectives within 1e-8, against the oracle."""
+    prob = P.generate_flow_lp(3, nodes=1 << 9, out_degree=4, commodities=6)
+    dev = _dev(prob)
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 1.0, lam)
+    dev.state_reset()
+    dev.run_inner(80, 0, 0, 1.0, lam, 2)
+    for _ in range(80):
+        O.iterate_once(st, slp)
+    assert np.array_equal(dev.to_host("y"), st.y)
+    assert np.array_equal(dev.to_host("x"), st.x)
+    cfg = dict(tolerance=1e-6, max_iterations=30000)
+    rep = P.solve(prob, P.SolverConfig(**cfg))
+    ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(**cfg))
+    assert rep.status.value == ref["status"]
+    assert rep.iterations == ref["iterations"]
+    assert [e.trigger for e in rep.restart_log] == [e["trigger"] for e in ref["restart_log"]]
+    assert _close(rep.primal_objective, ref["primal_objective"])
+    assert _close(rep.dual_objective, ref["dual_objective"])
