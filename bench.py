@@ -461,7 +461,7 @@ def run_c5(args, dist, ws, rank, local):
             "metric": "hpr_lp_iterations_per_sec", "value": value, "unit": "LP-it/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
                        "lps_per_rank": hi - lo, "lps_total": C5_COUNT,

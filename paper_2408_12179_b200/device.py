@@ -83,7 +83,7 @@ def _csr_parts(problem):
 class DeviceLP:
     """Uploads a reference-shaped LpProblem and owns its native context."""
 
-    def __init__(self, problem, device: int = 0, stream=None, pinned_upload: bool = True):
+    def __init__(self, problem, device: int = 0, stream=None):
         parts = _csr_parts(problem)
         m1 = int(problem.a_eq.nrows)
         m = m1 + int(problem.a_ineq.nrows)
@@ -114,7 +114,7 @@ class DeviceLP:
 
     @classmethod
     def from_arrays(cls, ro, ci, v, m, n, m1, b, c, lower, upper, *, device: int = 0,
-                    stream=None, n_alloc: int | None = None, pinned_upload: bool = True):
+                    stream=None, n_alloc: int | None = None):
         """A row block [rows of A, all n columns] (row-block mode): column vectors
         are allocated at ``n_alloc >= n`` (the group's padded length)."""
         self = cls.__new__(cls)

@@ -1,10 +1,15 @@
 #!/bin/bash
-# per-iteration timing of each built variant on C2 and C3
+# A/B timing of the variants built by scripts/build_variants.sh (same box, same
+# call: compare within one run only -- box-to-box variance is ~10-20 %).
+#   usage (under gpurun): bash scripts/gpu_variants.sh [configs...]   default: c2 c3
 mkdir -p gpurun_out
 out=gpurun_out/variants.log; : > $out
-for cfg in c2 c3; do
-  for so in paper_2408_12179_b200/variants/*.so; do
-    echo "== $cfg $(basename $so)" >> $out
-    HPR_LIB_PATH=$PWD/$so timeout 600 python scripts/prof_iter.py --config $cfg --reps 3 2>&1 | grep per-it >> $out
+cfgs=${@:-c2 c3}
+for rep in 1 2; do
+  for cfg in $cfgs; do
+    for so in paper_2408_12179_b200/variants/*.so; do
+      echo "== $cfg $(basename $so)" >> $out
+      HPR_LIB_PATH=$PWD/$so timeout 600 python scripts/prof_iter.py --config $cfg --reps 3 >> $out 2>&1
+    done
   done
 done
