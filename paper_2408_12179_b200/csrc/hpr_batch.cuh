@@ -95,6 +95,26 @@ __device__ __forceinline__ double srow(const int *rp, const int *ci, const doubl
   return s;
 }
 
+// two rows at once (independent chains interleaved: twice the shared-memory
+// loads in flight per thread); each row still summed left to right.  r1 < 0: none
+__device__ __forceinline__ void srow2(const int *rp, const int *ci, const double *val,
+                                      const double *v, int r0, int r1, double &s0, double &s1) {
+  s0 = 0.0;
+  s1 = 0.0;
+  int e0 = rp[r0], e1 = r1 >= 0 ? rp[r1] : 0;
+  const int z0 = rp[r0 + 1], z1 = r1 >= 0 ? rp[r1 + 1] : 0;
+  while (e0 < z0 && e1 < z1) {
+    const double p0 = __dmul_rn(val[e0], v[ci[e0]]);
+    const double p1 = __dmul_rn(val[e1], v[ci[e1]]);
+    s0 = __dadd_rn(s0, p0);
+    s1 = __dadd_rn(s1, p1);
+    ++e0;
+    ++e1;
+  }
+  for (; e0 < z0; ++e0) s0 = __dadd_rn(s0, __dmul_rn(val[e0], v[ci[e0]]));
+  for (; e1 < z1; ++e1) s1 = __dadd_rn(s1, __dmul_rn(val[e1], v[ci[e1]]));
+}
+
 // same for a global-memory CSR (original values at checkpoints); v in global
 // memory written earlier by this CTA (plain coherent loads, no __ldg)
 __device__ __forceinline__ double grow(const int *rp, int base, const int *ci, const double *val,
@@ -398,8 +418,15 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       }
       const double wn = wtab[2 * (st % kWTab)], wa = wtab[2 * (st % kWTab) + 1];
       int bad = 0;
-      for (int j = tid; j < n; j += kBT) {       // x phase (core.py:168-169)
-        const double aty = srow(atrp, atci, atv, y, j);
+      for (int j = tid; j < n; j += 2 * kBT) {   // x phase (core.py:168-169), 2 columns
+        const int j2 = j + kBT < n ? j + kBT : -1;
+        double aty0, aty1;
+        srow2(atrp, atci, atv, y, j, j2, aty0, aty1);
+        for (int h = 0; h < 2; ++h) {
+        const int jj = h ? j2 : j;
+        if (jj < 0) break;
+        const double aty = h ? aty1 : aty0;
+        const int j = jj;
         const double xj = x[j];
         const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
         const double xbj = np_clip(v, ls[j], us[j]);
@@ -409,6 +436,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
         w[j] = wj;
         x[j] = xn;
         bad |= !isfinite(xn);
+        }
       }
       __syncthreads();
       for (int i = tid; i < m; i += kBT) {       // y phase (core.py:170-172)
