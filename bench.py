@@ -157,13 +157,16 @@ def cpu_threads():
 # CPU reference arm / cpu_baseline (the oracle port; test infrastructure)
 # ---------------------------------------------------------------------------
 
-def _oracle_setup(prob):
+def _oracle_setup(prob, power_max=5000):
     from oracle import hprlp_oracle as O
     lib = O.load_clib()
     threads = lib.orc_set_threads(cpu_threads()) if lib is not None else 1
     lp = O.OracleLP.from_problem(prob)
     scaled, _ = O.scale_lp(lp)
-    est = O.power_lambda(scaled)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")        # a capped power method (C4 sample) warns
+        est = O.power_lambda(scaled, max_iters=power_max)
     st = O.State(y=np.zeros(scaled.m), x=np.zeros(scaled.n), ay=np.zeros(scaled.m),
                  ax=np.zeros(scaled.n), sigma=1.0, lam=est.value)
     return O, scaled, st, threads
@@ -247,10 +250,12 @@ def run_reference(args):
                          b_eq=b[:m1], b_ineq=b[m1:], c=c, lower=lo, upper=up)
         interval = 2
         tol = 1e-8
+        power_max = 3          # per-iteration time does not depend on lambda's accuracy
     else:
         prob, tol = make_instance(args.config)
         interval = 150
-    O, scaled, st, threads = _oracle_setup(prob)
+        power_max = 5000
+    O, scaled, st, threads = _oracle_setup(prob, power_max)
 
     def step():
         for _ in range(interval):
