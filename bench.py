@@ -74,6 +74,20 @@ def load_traffic(config):
     return None
 
 
+def gather_roofline(nnz, iterations, seconds):
+    """Operand gathers per second against one L1TEX wavefront per cycle per SM
+    (148 SMs at the max SM clock): 2 nnz gathers per HPR iteration."""
+    import torch
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    mhz = float(json.load(open(p)).get("sm_max_mhz", 1965.0)) if os.path.exists(p) else 1965.0
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    peak = sms * mhz * 1e6
+    achieved = 2.0 * nnz * iterations / seconds
+    return {"bound": "l1tex", "achieved": achieved, "peak": peak, "unit": "gathers/s",
+            "frac": achieved / peak,
+            "note": "2*nnz random fp64 operand gathers per iteration, 1 L1TEX wavefront each"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -408,6 +422,9 @@ def run_ours(args):
                          "kernel": "k_sell<EpiXIter> + k_sell<EpiYIter> (one HPR iteration)",
                          "bytes_per_iteration": bi, "peak_source": peak_kind,
                          "timing": "CUDA events around each 150-iteration graph replay"},
+            # the bound that actually binds a small-n problem (C2): every nonzero
+            # is one random 8-byte operand gather = one L1TEX wavefront per cycle per SM
+            "roofline_gather": gather_roofline(nnz, its_total, iter_s_total),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
