@@ -20,7 +20,7 @@ import numpy as np
 from . import _native as N
 from .driver import (KktResidual, RestartEvent, SolveReport, SolverConfig, SolveStatus, Timings,
                      Variant)
-from .problem import PrimalDualPoint, stacked_arrays
+from .problem import PrimalDualPoint
 
 _STATUS = {0: SolveStatus.OPTIMAL, 1: SolveStatus.ITERATION_LIMIT, 2: SolveStatus.TIME_LIMIT,
            3: SolveStatus.NUMERICAL_ERROR}
@@ -35,44 +35,65 @@ def _torch():
 
 
 class PackedBatch:
-    """Host-side concatenation of a list of reference-shaped LPs."""
+    """Host-side concatenation of a list of reference-shaped LPs (sizes first,
+    then every LP's arrays copied into preallocated batch arrays)."""
 
     def __init__(self, problems):
         if not problems:
             raise ValueError("empty batch")
-        rps, cis, vals, bs, cs, ls, us = [], [], [], [], [], [], []
-        ms, ns, nzs, m1s, oc, neg = [], [], [], [], [], []
-        for p in problems:
-            ro, ci, v, m, n, m1 = stacked_arrays(p)
-            if int(ro[-1]) == 0:
+        cnt = len(problems)
+        ms = np.empty(cnt, np.int64)
+        ns = np.empty(cnt, np.int64)
+        nzs = np.empty(cnt, np.int64)
+        m1s = np.empty(cnt, np.int32)
+        oc = np.empty(cnt, np.float64)
+        neg = np.empty(cnt, np.int32)
+        for i, p in enumerate(problems):
+            top, bot = p.a_eq, p.a_ineq
+            m1s[i] = int(top.nrows)
+            ms[i] = int(top.nrows) + int(bot.nrows)
+            ns[i] = int(top.ncols)
+            nzs[i] = (int(top.row_offsets[-1]) - int(top.row_offsets[0]) +
+                      int(bot.row_offsets[-1]) - int(bot.row_offsets[0]))
+            if nzs[i] == 0:
                 raise ValueError("matrix must be non-zero")
-            rps.append(np.asarray(ro, np.int32))
-            cis.append(np.asarray(ci, np.int32))
-            vals.append(np.asarray(v, np.float64))
-            bs.append(np.concatenate([np.asarray(p.b_eq, np.float64),
-                                      np.asarray(p.b_ineq, np.float64)]))
-            cs.append(np.asarray(p.c, np.float64))
-            ls.append(np.asarray(p.lower, np.float64))
-            us.append(np.asarray(p.upper, np.float64))
-            ms.append(m)
-            ns.append(n)
-            nzs.append(int(ro[-1]))
-            m1s.append(m1)
-            oc.append(float(getattr(p, "objective_constant", 0.0)))
-            neg.append(int(bool(getattr(p, "objective_negated", False))))
-        self.count = len(problems)
-        self.m = np.asarray(ms, np.int64)
-        self.n = np.asarray(ns, np.int64)
-        self.nnz = np.asarray(nzs, np.int64)
-        self.row_off = np.concatenate([[0], np.cumsum(self.m)]).astype(np.int64)
-        self.col_off = np.concatenate([[0], np.cumsum(self.n)]).astype(np.int64)
-        self.nz_off = np.concatenate([[0], np.cumsum(self.nnz)]).astype(np.int64)
+            oc[i] = float(getattr(p, "objective_constant", 0.0))
+            neg[i] = int(bool(getattr(p, "objective_negated", False)))
+        self.count = cnt
+        self.m, self.n, self.nnz = ms, ns, nzs
+        self.row_off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int64)
+        self.col_off = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
+        self.nz_off = np.concatenate([[0], np.cumsum(nzs)]).astype(np.int64)
+        R, C, Z = int(self.row_off[-1]), int(self.col_off[-1]), int(self.nz_off[-1])
+        rp = np.empty(R + cnt, np.int64)           # cast to int32 once, vectorised
+        ci = np.empty(Z, np.int64)
+        val = np.empty(Z, np.float64)
+        b = np.empty(R, np.float64)
+        c = np.empty(C, np.float64)
+        lo = np.empty(C, np.float64)
+        up = np.empty(C, np.float64)
+        for i, p in enumerate(problems):
+            r0, c0, z0 = int(self.row_off[i]), int(self.col_off[i]), int(self.nz_off[i])
+            top, bot = p.a_eq, p.a_ineq
+            mt, mb, n = int(top.nrows), int(bot.nrows), int(ns[i])
+            tro, bro = np.asarray(top.row_offsets), np.asarray(bot.row_offsets)
+            nt = int(tro[-1] - tro[0])
+            q = r0 + i                               # LP i's m + 1 row pointers
+            rp[q:q + mt + 1] = tro - tro[0]
+            rp[q + mt:q + mt + mb + 1] = bro - bro[0] + nt
+            ci[z0:z0 + nt] = top.col_indices
+            ci[z0 + nt:z0 + int(nzs[i])] = bot.col_indices
+            val[z0:z0 + nt] = top.values
+            val[z0 + nt:z0 + int(nzs[i])] = bot.values
+            b[r0:r0 + mt] = p.b_eq
+            b[r0 + mt:r0 + mt + mb] = p.b_ineq
+            c[c0:c0 + n] = p.c
+            lo[c0:c0 + n] = p.lower
+            up[c0:c0 + n] = p.upper
         self.arrays = {
             "row_off": self.row_off, "col_off": self.col_off, "nz_off": self.nz_off,
-            "m1": np.asarray(m1s, np.int32), "rp": np.concatenate(rps),
-            "ci": np.concatenate(cis), "val": np.concatenate(vals), "b": np.concatenate(bs),
-            "c": np.concatenate(cs), "lower": np.concatenate(ls), "upper": np.concatenate(us),
-            "obj_const": np.asarray(oc, np.float64), "obj_neg": np.asarray(neg, np.int32)}
+            "m1": m1s, "rp": rp.astype(np.int32), "ci": ci.astype(np.int32), "val": val, "b": b, "c": c, "lower": lo, "upper": up,
+            "obj_const": oc, "obj_neg": neg}
 
     def h2d_bytes(self):
         return sum(a.nbytes for a in self.arrays.values())

@@ -263,6 +263,7 @@ struct hpr_group {
   cudaGraphExec_t pow_graph = nullptr;
   bool inner_timed = false, ckpt_timed = false;
 
+  bool single = false;             // one rank, no collectives on the column vectors
   int gr(int l) const { return rank0 + l; }    // global rank of local rank l
   int owned() const { return (int)(K * cw); }
 };
@@ -279,6 +280,7 @@ PtrSet ptrs(hpr_group *g, double *RbRank::*f) {
 int g_reduce_scatter(hpr_group *g, cudaStream_t st = nullptr, int i0 = 0, int i1 = -1) {
   if (!st) st = g->stream;
   if (i1 < 0) i1 = g->K;
+  if (g->single) return HPR_OK;            // one rank: xslice aliases xpart
   if (g->use_nccl) {
     for (int i = i0; i < i1; ++i)
       NK(nccl().reduceScatter(g->r[0].xpart + (size_t)i * g->CW, g->r[0].xslice + (size_t)i * g->cw,
@@ -304,6 +306,7 @@ template <class VecOf>
 int g_all_gather(hpr_group *g, VecOf vec, cudaStream_t st = nullptr, int i0 = 0, int i1 = -1) {
   if (!st) st = g->stream;
   if (i1 < 0) i1 = g->K;
+  if (g->single) return HPR_OK;            // one rank owns every column
   if (g->use_nccl) {
     double *v = vec(0);
     for (int i = i0; i < i1; ++i)
@@ -395,7 +398,7 @@ int g_cols(hpr_group *g, int l, const Epi &epi, double *part, int *grid_out,
   if (!st) st = c->stream;
   if (i1 < 0) i1 = g->K;
   const int cnt = (i1 - i0) * (int)g->cw;
-  const int grid = std::max(1, std::min(grid_for(std::max(cnt, 1), kThreads), c->num_sms * 4));
+  const int grid = std::max(1, std::min(grid_for(std::max(cnt, 1), kThreads), c->num_sms * 16));
   k_cols<Epi><<<grid, kThreads, 0, st>>>(g->gr(l), (int)g->cw, (int)g->CW, i0, i1, (int)g->n,
                                          g->r[l].xslice, epi, part);
   CKL();
@@ -552,6 +555,10 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
   g->CW = g->cw * nranks;
   g->stream = ctxs[0]->stream;
   g->use_nccl = use_nccl;
+  {
+    const char *force = getenv("HPR_RB_NCCL_P1");
+    g->single = nranks == 1 && !(use_nccl && force && force[0] == '1');
+  }
   for (int l = 0; l < nlocal; ++l) {
     RbRank rr;
     rr.c = ctxs[l];
@@ -560,6 +567,10 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
     rr.xslice = (double *)(w + o_xslice);
     rr.gath = (double *)(w + o_gath);
     rr.row0 = row0[l];
+    // one rank owns every column in order: the reduced slice IS the partial
+    // (HPR_RB_NCCL_P1=1 keeps the NCCL calls at world size 1, for tests)
+    const char *force = getenv("HPR_RB_NCCL_P1");
+    if (nranks == 1 && !(use_nccl && force && force[0] == '1')) rr.xslice = rr.xpart;
     g->r.push_back(rr);
     // the partial's padding rows (n .. npad) are never written: keep them 0
     cudaMemsetAsync(rr.xpart, 0, sizeof(double) * g->npad, g->stream);

@@ -139,6 +139,7 @@ def test_nccl_transport_world1(golden_reports, chunks, monkeypatch):
     chunked NCCL reduce-scatter / all-gather) -- with one rank the collectives
     are copies, but the captured multi-stream graph is the P-GPU one."""
     monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
+    monkeypatch.setenv("HPR_RB_NCCL_P1", "1")      # keep the NCCL collectives at one rank
     import torch
     import torch.distributed as dist
     from paper_2408_12179_b200 import _native as N
