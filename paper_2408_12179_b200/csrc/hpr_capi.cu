@@ -48,6 +48,9 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_PDL
 #define HPR_PDL 0       // programmatic dependent launch between inner-loop phases (measured: no gain in graphs)
 #endif
+#ifndef HPR_L2KEEP
+#define HPR_L2KEEP 4    // matrix L2 policy: 0 evict_first, 1 keep A, 2 keep A^T, 3 normal, 4 auto
+#endif
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
@@ -99,7 +102,44 @@ bool cb_wanted(int64_t rows, int64_t cols, int64_t nnz) {
   return t_cb < 0.8 * t_sell;
 }
 
+// Column-split layout of A for the y-phase (hpr_kernels.cuh: EpiCarry): when
+// the gathered n-vector is larger than L2 and the rows are long enough that
+// the carried running sums (16 B per row per extra block) cost far less than
+// the HBM sectors the random gathers would miss on, the columns are cut into
+// NB blocks of W columns (W * 8 B = 32 MB stays L2-resident while every row
+// walks that block).  HPR_SPLIT=0 disables it, HPR_SPLIT_COLS=<W> forces it.
+constexpr int64_t kSplitCols = 4 << 20;
+constexpr int kSplitMaxBlocks = 64;
+struct SplitOff {
+  bool on = false;
+  int NB = 1, W = 0, m_pad = 0;
+  int64_t V = 0;                 // virtual rows NB * m_pad
+  PlanOff po;
+  size_t vrp = 0, psum = 0;
+};
+SplitOff split_plan_of(const hpr_dims &d) {
+  SplitOff o;
+  if (d.m < 1 || d.n < 1 || d.nnz < 1) return o;
+  const char *env = getenv("HPR_SPLIT");
+  if (env && env[0] == '0') return o;
+  int64_t W = kSplitCols;
+  const char *wc = getenv("HPR_SPLIT_COLS");
+  const bool forced = wc && atoll(wc) > 0;
+  if (forced) W = atoll(wc);
+  const int64_t NB = (d.n + W - 1) / W;
+  if (NB < 2 || NB > kSplitMaxBlocks) return o;
+  if (!forced && (double)d.nnz < 16.0 * (double)(NB - 1) * (double)d.m) return o;
+  o.on = true;
+  o.NB = (int)NB;
+  o.W = (int)W;
+  o.m_pad = (int)(windows_of(d.m) * kWindow);
+  o.V = (int64_t)o.NB * o.m_pad;
+  if (o.V >= INT_MAX - kWindow) o.on = false;
+  return o;
+}
+
 struct Layout {
+  SplitOff sp;
   PlanOff pa, pat;
   CbOff ca, cat;
   size_t cb_key = 0, cb_lrow = 0;
@@ -111,12 +151,15 @@ int cub_temp_bytes(const hpr_dims &d, size_t *bytes) {
   size_t s1 = 0, s2 = 0, s3 = 0;
   const int nnz = (int)d.nnz;
   const int nmax = (int)std::max(d.m, d.n);
-  const int smax = (int)(windows_of(nmax) * (kWindow / kSlice) + 1);
+  const SplitOff sp = split_plan_of(d);
+  const int smax = (int)std::max<int64_t>(windows_of(nmax) * (kWindow / kSlice) + 1,
+                                          sp.on ? sp.V + 1 : 0);
   CK(cub::DeviceRadixSort::SortPairs(nullptr, s1, (const int *)nullptr, (int *)nullptr,
                                      (const int *)nullptr, (int *)nullptr, nnz, 0, 32));
   CK(cub::DeviceScan::ExclusiveSum(nullptr, s2, (const int *)nullptr, (int *)nullptr, smax));
   CK(cub::DeviceSelect::Flagged(nullptr, s3, cub::CountingInputIterator<int>(0),
-                                (const int *)nullptr, (int *)nullptr, (int *)nullptr, nmax));
+                                (const int *)nullptr, (int *)nullptr, (int *)nullptr,
+                                std::max<int64_t>(nmax, sp.V)));
   *bytes = std::max(s1, std::max(s2, s3));
   return HPR_OK;
 }
@@ -144,6 +187,12 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
   };
   L.pa = plan(d.m);
   L.pat = plan(d.n);
+  L.sp = split_plan_of(d);
+  if (L.sp.on) {
+    L.sp.po = plan(L.sp.V);
+    L.sp.vrp = take(sizeof(int) * (L.sp.V + 1));
+    L.sp.psum = take(sizeof(double) * d.m);
+  }
   auto cbplan = [&](int64_t rows, int64_t cols) {
     CbOff o;
     o.on = cb_wanted(rows, cols, d.nnz);
@@ -213,6 +262,13 @@ struct hpr_ctx {
   char *ws = nullptr;
   Layout L{};
   Sell sa, sat;
+  struct Split {
+    bool on = false;
+    int NB = 1, W = 0, m_pad = 0, S_m = 0;   // S_m: slices per block
+    int *vrp = nullptr;
+    double *psum = nullptr;
+    Sell S;
+  } sp;
   struct Cb {
     bool on = false;
     int G = 0, NB = 0, rows_cap = 0, seg_cap = 0, smem = 0, stages = 2;
@@ -228,6 +284,7 @@ struct hpr_ctx {
   PowState *pow = nullptr;
   unsigned int *flags = nullptr;
   int bounds_uniform = 0;          // see EpiXIter
+  int keep_a = 0, keep_at = 0;     // L2 policy of the A / A^T streams (SellMat::keep)
   double lo_u = 0.0, up_u = 0.0;
   double *h_results = nullptr;       // pinned
   IterParams *h_params = nullptr;    // pinned
@@ -242,17 +299,30 @@ struct hpr_ctx {
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
     const int ga = S.nslices > 0 && S.slots >= (long long)HPR_GA_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
-                   S.long_rows, S.nslices, S.nlong, ga};
+                   S.long_rows, S.nslices, S.nlong, ga, 0};
   }
   CbMat cbmat(const Cb &C, int ncols) const {
     return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
                  C.rows_cap, C.seg_cap, C.stages};
   }
   SellMat mat_a(bool scaled) const {
-    return mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
+    SellMat M = mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
+    M.keep = keep_a;
+    return M;
+  }
+  // block b of the column-split A (scaled values; iteration y-phase only)
+  SellMat mat_split(int b) const {
+    const Sell &S = sp.S;
+    const size_t so = (size_t)b * sp.S_m;
+    SellMat M{S.slice_ptr + so, S.slice_row + so * kSlice, S.slice_len + so * kSlice, S.ci, S.val_s,
+              nullptr, nullptr, nullptr, nullptr, sp.S_m, 0, 0, keep_a};
+    M.ga = (long long)(S.slots) >= (long long)HPR_GA_MIN * 32 * S.nslices;
+    return M;
   }
   SellMat mat_at(bool scaled) const {
-    return mat(sat, B.at_rp, B.at_ci, scaled ? B.at_val_s : B.at_val, scaled);
+    SellMat M = mat(sat, B.at_rp, B.at_ci, scaled ? B.at_val_s : B.at_val, scaled);
+    M.keep = keep_at;
+    return M;
   }
 };
 
@@ -299,6 +369,24 @@ int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, 
               : launch_sell_u<4, false>(c, M, xg, epi, part, grid_out, pdl);
 }
 
+// The y-phase product A w with the phase epilogue: one SELL launch, or NB
+// launches over the column-split layout carrying the running sums.
+template <class Epi>
+int launch_a_iter(hpr_ctx *c, const double *wg, const Epi &epi, bool pdl) {
+  if (!c->sp.on) return launch_sell(c, c->mat_a(true), wg, epi, nullptr, nullptr, pdl);
+  for (int b = 0; b + 1 < c->sp.NB; ++b) {
+    EpiCarry ec{};
+    ec.psum = c->sp.psum;
+    ec.first = b == 0;
+    int rc = launch_sell(c, c->mat_split(b), wg, ec, nullptr, nullptr, pdl && b == 0);
+    if (rc) return rc;
+  }
+  EpiCarryIn<Epi> el{};
+  static_cast<Epi &>(el) = epi;
+  el.psum = c->sp.psum;
+  return launch_sell(c, c->mat_split(c->sp.NB - 1), wg, el, nullptr, nullptr, false);
+}
+
 // parts layout inside ctx->part (in doubles)
 struct Parts {
   double *xhalf, *yhalf, *merit, *krow, *kcol, *powt, *powa, *misc;
@@ -320,7 +408,8 @@ Parts parts_of(const hpr_ctx *c) {
 int sumsq_blocks(int64_t n) { return grid_for(n, kThreads, kSumsqBlocks); }
 
 // SELL plan of one matrix: slice order, slot offsets, long-row list
-int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) {
+int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
+              int long_thresh = kLongRow, int m_pad = 0, int m_real = 0) {
   S.nrows = nrows;
   const int nw = (int)windows_of(nrows);
   S.nslices = nw * (kWindow / kSlice);
@@ -334,7 +423,7 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) 
   cudaStream_t s = c->stream;
   CK(cudaMemsetAsync(S.slice_slots + S.nslices, 0, sizeof(int), s));
   k_sell_plan<<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots,
-                                     S.long_flag);
+                                     S.long_flag, long_thresh, m_pad, m_real);
   CKL();
   size_t tb = c->L.cub_bytes;
   CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, S.slice_slots, S.slice_ptr,
@@ -350,6 +439,67 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S) 
   if (total < 0) return fail(HPR_EINVAL, "SELL slot count overflows int32");
   S.slots = total;
   S.nlong = nl;
+  return HPR_OK;
+}
+
+// ---- column-split layout of A (SplitOff): plan at hpr_analyze ----
+int split_plan(hpr_ctx *c) {
+  hpr_ctx::Split &P = c->sp;
+  P = hpr_ctx::Split{};
+  const SplitOff &o = c->L.sp;
+  if (!o.on) return HPR_OK;
+  cudaStream_t s = c->stream;
+  P.NB = o.NB;
+  P.W = o.W;
+  P.m_pad = o.m_pad;
+  P.S_m = o.m_pad / kSlice;
+  P.vrp = (int *)(c->ws + o.vrp);
+  P.psum = (double *)(c->ws + o.psum);
+  k_split_count<<<grid_for(o.m_pad), 256, 0, s>>>(c->B.a_rp, c->B.a_ci, (int)c->d.m, o.m_pad, o.W,
+                                                  o.NB, P.vrp);
+  CKL();
+  CK(cudaMemsetAsync(P.vrp + o.V, 0, sizeof(int), s));
+  size_t tb = c->L.cub_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, P.vrp, P.vrp, (int)o.V + 1, s));
+  c->launches += 2;
+  // every virtual row stays in the slices (lengths <= 65535); otherwise no split
+  int rc = plan_sell(c, o.po, P.vrp, (int)o.V, P.S, 65535, o.m_pad, (int)c->d.m);
+  if (rc) return rc;
+  if (P.S.nlong > 0) {
+    P = hpr_ctx::Split{};
+    return HPR_OK;
+  }
+  P.on = true;
+  return HPR_OK;
+}
+
+size_t split_bytes(const hpr_ctx::Split &P, int64_t nnz) {
+  if (!P.on) return 0;
+  return align_up((size_t)P.S.slots * 4 + 256, 256) + align_up((size_t)P.S.slots * 8 + 256, 256) +
+         align_up((size_t)nnz * 4 + 256, 256);
+}
+
+// ---- column-split layout: fill at hpr_bind_layout (scaled values at hpr_scale) ----
+int split_layout(hpr_ctx *c, char *&p) {
+  hpr_ctx::Split &P = c->sp;
+  if (!P.on) return HPR_OK;
+  Sell &S = P.S;
+  const long long nnz = c->d.nnz;
+  cudaStream_t s = c->stream;
+  S.ci = (int *)p;
+  p += align_up((size_t)S.slots * 4 + 256, 256);
+  S.val_s = (double *)p;
+  p += align_up((size_t)S.slots * 8 + 256, 256);
+  S.pos = (int *)p;
+  p += align_up((size_t)nnz * 4 + 256, 256);
+  S.val0 = nullptr;
+  CK(cudaMemsetAsync(S.ci, 0, (size_t)S.slots * 4, s));
+  CK(cudaMemsetAsync(S.val_s, 0, (size_t)S.slots * 8, s));
+  CK(cudaMemsetAsync(S.pos, 0xff, (size_t)nnz * 4, s));
+  k_split_fill<<<grid_for((int64_t)S.nslices * 32), 256, 0, s>>>(
+      c->B.a_rp, c->B.a_ci, P.vrp, S.slice_ptr, S.slice_row, S.nslices, P.m_pad, P.W, S.ci, S.pos);
+  CKL();
+  c->launches += 1;
   return HPR_OK;
 }
 
@@ -737,8 +887,10 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   if (rc) return rc;
   rc = cb_plan(c, c->L.cat, B.at_rp, B.at_ci, n, c->cbat);
   if (rc) return rc;
+  rc = split_plan(c);
+  if (rc) return rc;
   *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz) +
-                  cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz);
+                  cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz) + split_bytes(c->sp, d.nnz);
   c->analyzed = true;
   c->laid_out = false;
   return HPR_OK;
@@ -750,7 +902,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (!c->analyzed) return fail(HPR_ESTATE, "hpr_analyze has not been called");
   if (!layout) return fail(HPR_EINVAL, "null layout");
   if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz) +
-                  cb_bytes(c->cba, c->d.nnz) + cb_bytes(c->cbat, c->d.nnz))
+                  cb_bytes(c->cba, c->d.nnz) + cb_bytes(c->cbat, c->d.nnz) +
+                  split_bytes(c->sp, c->d.nnz))
     return fail(HPR_EINVAL, "layout buffer too small");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
@@ -763,13 +916,16 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (rc) return rc;
   rc = cb_layout(c, p, c->cbat, B.at_rp, B.at_ci);
   if (rc) return rc;
+  rc = split_layout(c, p);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(c->stream));
   // the captured graphs hold the layout's pointers and the plans' counts: keep
   // them when a re-analysed problem reproduces both (a re-solve of the same
   // structure), drop them otherwise
   std::vector<long long> sig = {(long long)(uintptr_t)layout, (long long)bytes};
-  for (const Sell *S : {&c->sa, &c->sat})
+  for (const Sell *S : {&c->sa, &c->sat, &c->sp.S})
     for (long long v : {(long long)S->nslices, S->slots, (long long)S->nlong}) sig.push_back(v);
+  for (long long v : {(long long)c->sp.on, (long long)c->sp.NB, (long long)c->sp.W}) sig.push_back(v);
   for (const hpr_ctx::Cb *C : {&c->cba, &c->cbat})
     for (long long v : {(long long)C->on, (long long)C->G, (long long)C->NB, (long long)C->rows_cap,
                         (long long)C->seg_cap, (long long)C->stages, C->npad, C->nrpb})
@@ -782,6 +938,23 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
       c->pow_graph = nullptr;
     }
     c->graph_sig = sig;
+  }
+  c->keep_a = c->keep_at = 0;
+  {
+    // L2 policy of the matrix streams (SellMat::keep)
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+    const double a_bytes = 12.0 * (double)c->sa.slots, at_bytes = 12.0 * (double)c->sat.slots;
+    switch (HPR_L2KEEP) {
+      case 1: c->keep_a = 1; break;
+      case 2: c->keep_at = 1; break;
+      case 3: c->keep_a = c->keep_at = 2; break;
+      case 4:
+        if (at_bytes <= 0.6 * l2) c->keep_at = 1;
+        else if (a_bytes <= 0.6 * l2) c->keep_a = 1;
+        break;
+      default: break;
+    }
   }
   c->laid_out = true;
   c->scaled = false;
@@ -850,8 +1023,9 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
     k_gather_vals<<<grid_for(nnz), 256, 0, s>>>(B.at_perm, B.a_val_s, B.at_val_s, nnz);
     k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sa.pos, B.a_val_s, c->sa.val_s, nnz);
     k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sat.pos, B.at_val_s, c->sat.val_s, nnz);
+    if (c->sp.on) k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sp.S.pos, B.a_val_s, c->sp.S.val_s, nnz);
     CKL();
-    c->launches += 3;
+    c->launches += 3 + (int)c->sp.on;
     if (c->cba.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cba.pos, B.a_val_s, c->cba.val, nnz);
     if (c->cbat.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cbat.pos, B.at_val_s, c->cbat.val, nnz);
     CKL();
@@ -1061,7 +1235,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
                            : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
       if (!rc2)
         rc2 = c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
-                        : launch_sell(c, A, B.w, ey, nullptr, nullptr, true);
+                        : launch_a_iter(c, B.w, ey, true);
       if (rc2) {
         cudaStreamEndCapture(s, &g);
         return rc2;
@@ -1082,7 +1256,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
   CK(cudaGraphLaunch(it->second, s));
   CK(cudaEventRecord(c->ev1, s));
   c->inner_timed = true;
-  c->launches += 1 + 2LL * steps;
+  c->launches += 1 + (1LL + (c->sp.on ? c->sp.NB : 1)) * steps;
   return HPR_OK;
 }
 
@@ -1222,6 +1396,7 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->long_rows_at = c->sat.nlong;
   info->cb_a = c->cba.on ? c->cba.npad : 0;
   info->cb_at = c->cbat.on ? c->cbat.npad : 0;
+  info->split_a = c->sp.on ? c->sp.NB : 0;
   return HPR_OK;
 }
 

@@ -21,6 +21,9 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+#include <utility>
+
 namespace hpr {
 
 constexpr int kThreads = 128;           // CTA size of the SELL / reduction kernels
@@ -39,6 +42,17 @@ __device__ __forceinline__ double np_clip(double v, double l, double u) { return
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// a matrix small enough to stay in L2 between iterations (SellMat::keep)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ double ld_stream(const double *ptr, uint64_t pol) {
@@ -76,6 +90,7 @@ struct SellMat {
   int nslices;
   int nlong;
   int ga;                  // long rows: gather one batch ahead (HPR_GA_MIN)
+  int keep;                // L2 policy of the matrix streams: 0 evict_first, 1 evict_last, 2 normal
 };
 
 constexpr int kSlice = 32;
@@ -86,6 +101,9 @@ constexpr int kWarpsPerCta = kThreads / 32;
 #define HPR_UNROLL 4
 #endif
 
+#ifndef HPR_LATE_PREFETCH
+#define HPR_LATE_PREFETCH 0   // load the epilogue's row operands after the row's sum (fewer live registers)
+#endif
 constexpr int kUnroll = HPR_UNROLL;     // entries per lane in flight (x2: software pipelined)
 
 // Parameters of the inner iterations, resident in device memory so a captured
@@ -165,15 +183,26 @@ __device__ __forceinline__ SliceHdr load_hdr(const SellMat &M, int s, int lane) 
   return h;
 }
 
+// An epilogue with init(r) starts row r's running sum there instead of at 0.0
+// (column-split layout: the sum carried over from the previous column block).
+template <class E, class = void>
+struct has_init : std::false_type {};
+template <class E>
+struct has_init<E, std::void_t<decltype(std::declval<E &>().init(0))>> : std::true_type {};
+
 template <int U, bool GA, class Epi>
 __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
   const int row = h.row, len = h.len, slen = h.slen;
+#if !HPR_LATE_PREFETCH
   if (row >= 0) epi.prefetch(row);
+#endif
   const int *cp = M.ci + h.base + lane;
   const double *vp = M.val + h.base + lane;
   double sum = 0.0;
+  if constexpr (has_init<Epi>::value)
+    if (row >= 0) sum = epi.init(row);
   // software pipeline: the streaming loads of batch i+1 are in flight while
   // batch i's operand gathers complete and its products are added in order
   int c[U];
@@ -247,6 +276,9 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
     }
   }
   }
+#if HPR_LATE_PREFETCH
+  if (row >= 0) epi.prefetch(row);
+#endif
   if (row >= 0) epi.finish(row, sum, acc);
 }
 
@@ -329,7 +361,8 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
 #pragma unroll
   for (int q = 0; q < (Epi::NQ > 0 ? Epi::NQ : 1); ++q) acc[q] = 0.0;
   if (!epi.enter()) return;
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = M.keep == 1 ? policy_evict_last()
+                       : M.keep == 2 ? policy_evict_normal() : policy_evict_first();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int G = gridDim.x;
@@ -424,6 +457,27 @@ struct EpiYIter {
     y[i] = yn;
     if (!isfinite(yn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
   }
+};
+
+// Column-split layout (hpr_capi.cu: Split): A's columns are cut into NB blocks
+// small enough for the gathered vector's block to stay in L2; block b's
+// kernel continues every row's running sum from block b-1 (psum), so each row
+// is still summed in ascending column order from 0.0 -- bit-identical to the
+// unsplit product.  Blocks 0..NB-2 store the running sums, the last block
+// hands them to the phase's real epilogue (EpiCarryIn).
+struct EpiCarry {
+  static constexpr int NQ = 0;
+  double *psum;
+  int first;
+  __device__ bool enter() { return true; }
+  __device__ double init(int r) { return first ? 0.0 : psum[r]; }
+  __device__ void prefetch(int) {}
+  __device__ void finish(int r, double s, double *) { psum[r] = s; }
+};
+template <class Epi>
+struct EpiCarryIn : Epi {
+  const double *psum;
+  __device__ double init(int r) { return psum[r]; }
 };
 
 // ---------------------------------------------------------------------------
@@ -731,16 +785,20 @@ __global__ void k_gather_t(const int *perm, const int *row_of, const double *val
 // and the slot count of each slice (32 * longest row in it).
 __global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows, int sort_rows,
                                                        int *slice_row, unsigned short *slice_len,
-                                                       int *slice_slots, int *long_flag) {
+                                                       int *slice_slots, int *long_flag,
+                                                       int long_thresh, int m_pad, int m_real) {
   __shared__ int key[kWindow];
   __shared__ int skey[kWindow];
   const int t = threadIdx.x;
   const int r = blockIdx.x * kWindow + t;
   int k = -2;
-  if (r < nrows) {
+  // column-split plans (m_pad > 0): virtual rows b * m_pad + i with i >= m_real are padding
+  if (r < nrows && (m_pad == 0 || r % m_pad < m_real)) {
     const int len = rp[r + 1] - rp[r];
-    k = len > kLongRow ? -1 : len;
-    long_flag[r] = len > kLongRow;
+    k = len > long_thresh ? -1 : len;
+    long_flag[r] = len > long_thresh;
+  } else if (r < nrows) {
+    long_flag[r] = 0;
   }
   key[t] = k;
   __syncthreads();
@@ -753,7 +811,8 @@ __global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows,
     }
   }
   skey[rank] = k;
-  slice_row[blockIdx.x * kWindow + rank] = k >= 0 ? r : -1;
+  // column-split plans store the real row i of virtual row b * m_pad + i
+  slice_row[blockIdx.x * kWindow + rank] = k >= 0 ? (m_pad ? r % m_pad : r) : -1;
   slice_len[blockIdx.x * kWindow + rank] = (unsigned short)(k >= 0 ? k : 0);
   __syncthreads();
   if (t < kWindow / kSlice) {
@@ -776,6 +835,53 @@ __global__ void k_sell_fill(const int *rp, const int *ci, const int *slice_ptr,
       const int pos = base + k * kSlice + lane;
       sell_ci[pos] = ci[z0 + k];
       sell_pos[z0 + k] = pos;
+    }
+  }
+}
+
+// Column-split layout: entry counts of the virtual rows (b, i) = b * m_pad + i
+// (row i's entries with column in [b W, (b+1) W)); thread per row, columns ascend.
+__global__ void k_split_count(const int *rp, const int *ci, int nrows, int m_pad, int W, int NB,
+                              int *cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_pad; i += gridDim.x * blockDim.x) {
+    int k = i < nrows ? rp[i] : 0;
+    const int z1 = i < nrows ? rp[i + 1] : 0;
+    for (int b = 0; b < NB; ++b) {
+      const long long hi = (long long)(b + 1) * W;
+      int c0 = 0;
+      while (k < z1 && ci[k] < hi) {
+        ++k;
+        ++c0;
+      }
+      cnt[(long long)b * m_pad + i] = c0;
+    }
+  }
+}
+
+// Column-split layout: slot column indices and the CSR -> slot map (warp per
+// slice; a virtual row's entries are a contiguous run of its CSR row)
+__global__ void k_split_fill(const int *rp, const int *ci, const int *vrp, const int *slice_ptr,
+                             const int *slice_row, int nslices, int m_pad, int W, int *sell_ci,
+                             int *sell_pos) {
+  const int slices_per_block = m_pad / kSlice;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += nw) {
+    const int i = slice_row[s * kSlice + lane];
+    if (i < 0) continue;
+    const int b = s / slices_per_block, v = b * m_pad + i;
+    const int len = vrp[v + 1] - vrp[v], base = slice_ptr[s];
+    if (len == 0) continue;
+    const long long lo = (long long)b * W;
+    int a = rp[i], e = rp[i + 1];
+    while (a < e) {                        // first entry with column >= b W
+      const int mid = (a + e) >> 1;
+      if (ci[mid] < lo) a = mid + 1; else e = mid;
+    }
+    for (int k = 0; k < len; ++k) {
+      const int pos = base + k * kSlice + lane;
+      sell_ci[pos] = ci[a + k];
+      sell_pos[a + k] = pos;
     }
   }
 }

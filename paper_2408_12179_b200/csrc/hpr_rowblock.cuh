@@ -740,6 +740,8 @@ int hpr_group_scale(hpr_group *g, int ruiz_iters, int pock_chambolle, int bc_nor
       k_gather_vals<<<grid_for(nnz), 256, 0, c->stream>>>(B.at_perm, B.a_val_s, B.at_val_s, nnz);
       k_sell_scatter<<<grid_for(nnz), 256, 0, c->stream>>>(c->sa.pos, B.a_val_s, c->sa.val_s, nnz);
       k_sell_scatter<<<grid_for(nnz), 256, 0, c->stream>>>(c->sat.pos, B.at_val_s, c->sat.val_s, nnz);
+      if (c->sp.on)
+        k_sell_scatter<<<grid_for(nnz), 256, 0, c->stream>>>(c->sp.S.pos, B.a_val_s, c->sp.S.val_s, nnz);
       CKL();
       c->launches += 3;
     }
@@ -997,7 +999,7 @@ int hpr_group_run_inner(hpr_group *g, int steps, int64_t t, int64_t k, double si
         ey.P = c->params;
         ey.m1 = (int)c->d.m1;
         ey.step = i;
-        rc = launch_sell(c, c->mat_a(true), B.w, ey, nullptr, nullptr);
+        rc = launch_a_iter(c, B.w, ey, false);
       }
     }
     cudaError_t e = cudaStreamEndCapture(g->stream, &gr);
@@ -1026,7 +1028,9 @@ int hpr_group_run_inner(hpr_group *g, int steps, int64_t t, int64_t k, double si
   c0->inner_timed = true;
   // per step: nlocal x (A^T partial + slice epilogue + y phase) + the collectives
   const int coll = (g->P == 1 || g->use_nccl) ? 0 : 2;
-  c0->launches += g->nlocal + (long long)steps * (3 * g->nlocal + coll);
+  long long split_extra = 0;   // column-split y-phase: NB launches instead of one
+  for (int l = 0; l < g->nlocal; ++l) split_extra += g->r[l].c->sp.on ? g->r[l].c->sp.NB - 1 : 0;
+  c0->launches += g->nlocal + (long long)steps * (3 * g->nlocal + coll + split_extra);
   return HPR_OK;
 }
 

@@ -215,6 +215,7 @@ class RowBlockGroup:
     def layout_info(self) -> dict:
         infos = [b.layout_info() for b in self.blocks]
         out = {k: sum(i[k] for i in infos) for k in infos[0]}
+        out["split_a"] = max(i["split_a"] for i in infos)   # column blocks, not a count
         out["partitions"] = self.P
         return out
 

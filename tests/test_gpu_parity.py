@@ -67,17 +67,28 @@ def assert_report_parity(rep, g, name=""):
 # kernels: bit-exact against the oracle
 # ---------------------------------------------------------------------------
 
-ENGINES = {"sell": "0", "cb": "1"}   # HPR_CB: SELL-32-sigma / column-blocked smem-staged
+# SELL-32-sigma / column-blocked smem-staged (HPR_CB) / SELL with A's columns
+# split into blocks whose running sums are carried block to block (HPR_SPLIT_COLS)
+ENGINES = ["sell", "cb", "split"]
 
 
-@pytest.mark.parametrize("engine", list(ENGINES))
+def _engine_env(monkeypatch, engine, n):
+    monkeypatch.setenv("HPR_CB", "1" if engine == "cb" else "0")
+    if engine == "split":
+        monkeypatch.setenv("HPR_SPLIT_COLS", str(max(1, -(-n // 7))))   # 7 column blocks
+    else:
+        monkeypatch.setenv("HPR_SPLIT", "0")
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("variant,code", [("hpr", 2), ("hdr", 1), ("dr", 0)])
 def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
-    monkeypatch.setenv("HPR_CB", ENGINES[engine])
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    _engine_env(monkeypatch, engine, prob.n)
     dev = _dev(prob)
     info = dev.layout_info()
     assert (info["cb_a"] > 0 and info["cb_at"] > 0) == (engine == "cb")
+    assert info["split_a"] == (7 if engine == "split" else 0)
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.83, lam,
@@ -136,11 +147,10 @@ def test_c1_trajectory_vs_reference_golden():
         assert rel <= 1e-10, (k, rel)
 
 
-@pytest.mark.parametrize("engine", list(ENGINES))
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("shape", ["ineq_only", "eq_only", "empty_rows_cols", "long_rows",
                                    "one_by_one"])
 def test_edge_shapes_bit_exact(shape, engine, monkeypatch):
-    monkeypatch.setenv("HPR_CB", ENGINES[engine])
     rng = np.random.default_rng(7)
     if shape == "ineq_only":
         prob = P.LpProblem.from_dense(None, None, rng.uniform(-1, 1, (7, 5)), rng.uniform(-1, 0, 7),
@@ -177,7 +187,10 @@ def test_edge_shapes_bit_exact(shape, engine, monkeypatch):
                                       lower=np.zeros(n), upper=np.full(n, 3.0))
     else:
         prob = one_d_problem()
+    _engine_env(monkeypatch, engine, prob.n)
     dev = _dev(prob)
+    if engine == "split" and prob.n >= 7:
+        assert dev.layout_info()["split_a"] >= 2
     est = dev.power(1e-4, 5000)
     lam = est.raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)

@@ -74,6 +74,32 @@ def test_partition_one_is_bit_exact_with_single_context():
     dev.close()
 
 
+@pytest.mark.parametrize("parts,chunks", [(1, 1), (3, 1), (2, 3)])
+def test_partitioned_column_split_bit_exact(parts, chunks, monkeypatch):
+    """The column-split y-phase (A's columns in blocks, running sums carried
+    block to block) lands on the same bits as the unsplit one."""
+    monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    out = []
+    for split in ("0", "300"):
+        if split == "0":
+            monkeypatch.setenv("HPR_SPLIT", "0")
+            monkeypatch.delenv("HPR_SPLIT_COLS", raising=False)
+        else:
+            monkeypatch.delenv("HPR_SPLIT", raising=False)
+            monkeypatch.setenv("HPR_SPLIT_COLS", split)
+        grp = RowBlockGroup.local(prob, parts)
+        grp.analyze()
+        assert all((b.layout_info()["split_a"] == 7) == (split != "0") for b in grp.blocks)
+        grp.scale(10, True, True)
+        lam = grp.power(1e-4, 5000).raw * 1.001
+        grp.state_reset()
+        grp.run_inner(60, 0, 0, 0.9, lam * 0.9, 2)
+        out.append((grp.to_host("y"), grp.to_host("x")))
+        grp.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
 @pytest.mark.parametrize("parts", [2, 4])
 def test_partitioned_scaling_and_power(parts):
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
