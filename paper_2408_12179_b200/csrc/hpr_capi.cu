@@ -48,6 +48,9 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_PDL
 #define HPR_PDL 0       // programmatic dependent launch between inner-loop phases (measured: no gain in graphs)
 #endif
+#ifndef HPR_CARVEOUT
+#define HPR_CARVEOUT -1   // SELL kernels' preferred shared-memory carve-out (-1: driver default)
+#endif
 #ifndef HPR_L2KEEP
 #define HPR_L2KEEP 4    // matrix L2 policy: 0 evict_first, 1 keep A, 2 keep A^T, 3 normal, 4 auto
 #endif
@@ -132,7 +135,8 @@ SplitOff split_plan_of(const hpr_dims &d) {
   o.on = true;
   o.NB = (int)NB;
   o.W = (int)W;
-  o.m_pad = (int)(windows_of(d.m) * kWindow);
+  const int win = sort_win(d.m);     // windows never straddle two column blocks
+  o.m_pad = (int)((d.m + win - 1) / win * win);
   o.V = (int64_t)o.NB * o.m_pad;
   if (o.V >= INT_MAX - kWindow) o.on = false;
   return o;
@@ -335,6 +339,9 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
                   int *grid_out, bool pdl) {
   static int occ = 0;
   if (occ == 0) {
+    if (HPR_CARVEOUT >= 0)   // shared-memory carve-out: 0 = the whole unified array as L1
+      CK(cudaFuncSetAttribute(k_sell<U, GA, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              HPR_CARVEOUT));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, GA, Epi>, kThreads, 0));
     if (occ < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
     occ = std::min(occ, kMaxGridPerSm);
@@ -413,6 +420,7 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   S.nrows = nrows;
   const int nw = (int)windows_of(nrows);
   S.nslices = nw * (kWindow / kSlice);
+  const int win = sort_win(m_pad ? m_pad : nrows);   // split plans: the real row count
   S.slice_row = (int *)(c->ws + po.slice_row);
   S.slice_len = (unsigned short *)(c->ws + po.slice_len);
   S.slice_slots = (int *)(c->ws + po.slice_slots);
@@ -422,8 +430,14 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   S.nsel = (int *)(c->ws + po.nsel);
   cudaStream_t s = c->stream;
   CK(cudaMemsetAsync(S.slice_slots + S.nslices, 0, sizeof(int), s));
-  k_sell_plan<<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots,
-                                     S.long_flag, long_thresh, m_pad, m_real);
+  if (win == kSortWinBig)
+    k_sell_plan<kSortWinBig><<<(nrows + win - 1) / win, win, 0, s>>>(
+        rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots, S.long_flag, long_thresh, m_pad,
+        m_real);
+  else
+    k_sell_plan<kWindow><<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len,
+                                                S.slice_slots, S.long_flag, long_thresh, m_pad,
+                                                m_real);
   CKL();
   size_t tb = c->L.cub_bytes;
   CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, S.slice_slots, S.slice_ptr,

@@ -68,6 +68,21 @@ __device__ __forceinline__ int ld_stream(const int *ptr, uint64_t pol) {
   return v;
 }
 
+// Row operands of the iteration epilogues (read once per iteration): with
+// HPR_EPI_NA they bypass L1 allocation so the gathered vector keeps the L1.
+#ifndef HPR_EPI_NA
+#define HPR_EPI_NA 0
+#endif
+__device__ __forceinline__ double ld_epi(const double *ptr) {
+#if HPR_EPI_NA
+  double v;
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+#else
+  return *ptr;
+#endif
+}
+
 // Device layout of one matrix for the iteration kernels: SELL-32-sigma.
 // Rows are grouped in slices of 32 (lane i of a warp owns one row); inside a
 // window of kWindow rows they are ordered by decreasing length so a slice's
@@ -94,7 +109,20 @@ struct SellMat {
 };
 
 constexpr int kSlice = 32;
-constexpr int kWindow = kThreads;       // sigma: sorting window (= one CTA's 4 slices)
+constexpr int kWindow = kThreads;       // one CTA's 4 slices (the SELL kernels' work unit)
+// sigma: rows are sorted by length inside windows of sort_win(nrows) rows.
+// HPR_SORT_WIN=1024 for large matrices cuts slice padding (C4's A^T 28 % -> 4 %)
+// but measured slower (C2 57.1 vs 53.6 us, C4 1837 vs 1618 us per iteration):
+// a slice's 32 rows then spread over 1024 rows, so the epilogue's vector loads
+// and stores stop coalescing, and CTA windows get unequal work.  Default 128.
+#ifndef HPR_SORT_WIN
+#define HPR_SORT_WIN 128   // 1024 measured slower (C2 +6 %, C4 +13 %): uncoalesced epilogue rows
+#endif
+constexpr int kSortWinBig = HPR_SORT_WIN;
+constexpr long long kSortBigRows = 131072;
+__host__ __device__ inline int sort_win(long long nrows) {
+  return nrows >= kSortBigRows ? kSortWinBig : kWindow;
+}
 constexpr int kLongRow = 1024;
 constexpr int kWarpsPerCta = kThreads / 32;
 #ifndef HPR_UNROLL
@@ -408,11 +436,11 @@ struct EpiXIter {
     return true;
   }
   __device__ void prefetch(int j) {
-    xj = x[j];
-    cj = c[j];
-    lj = (bounds_uniform & 1) ? lo_u : lo[j];
-    uj = (bounds_uniform & 2) ? up_u : up[j];
-    aj = variant ? anc[j] : 0.0;
+    xj = ld_epi(x + j);
+    cj = ld_epi(c + j);
+    lj = (bounds_uniform & 1) ? lo_u : ld_epi(lo + j);
+    uj = (bounds_uniform & 2) ? up_u : ld_epi(up + j);
+    aj = variant ? ld_epi(anc + j) : 0.0;
   }
   __device__ void finish(int j, double aty, double *) {
     const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cj)));
@@ -442,9 +470,9 @@ struct EpiYIter {
     return true;
   }
   __device__ void prefetch(int i) {
-    yi = y[i];
-    bi = b[i];
-    ai = variant ? anc[i] : 0.0;
+    yi = ld_epi(y + i);
+    bi = ld_epi(b + i);
+    ai = variant ? ld_epi(anc + i) : 0.0;
   }
   __device__ void finish(int i, double s, double *) {
     double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bi, s), lamsig));
@@ -780,17 +808,20 @@ __global__ void k_gather_t(const int *perm, const int *row_of, const double *val
 
 
 
-// SELL plan: CTA per window of kWindow rows.  Rows are ranked by (length desc,
-// index asc); long rows and padding go last with row = -1.  Writes slice_row
-// and the slot count of each slice (32 * longest row in it).
-__global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows, int sort_rows,
-                                                       int *slice_row, unsigned short *slice_len,
-                                                       int *slice_slots, int *long_flag,
-                                                       int long_thresh, int m_pad, int m_real) {
-  __shared__ int key[kWindow];
-  __shared__ int skey[kWindow];
+// SELL plan: CTA per sorting window of WIN rows.  Rows are ranked by (length
+// desc, index asc); long rows and padding go last with row = -1.  Writes
+// slice_row and the slot count of each slice (32 * longest row in it); the
+// arrays cover nrows rounded up to kWindow (a last partial window stops there).
+template <int WIN>
+__global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int sort_rows,
+                                                   int *slice_row, unsigned short *slice_len,
+                                                   int *slice_slots, int *long_flag,
+                                                   int long_thresh, int m_pad, int m_real) {
+  __shared__ int key[WIN];
+  __shared__ int skey[WIN];
   const int t = threadIdx.x;
-  const int r = blockIdx.x * kWindow + t;
+  const int r = blockIdx.x * WIN + t;
+  const int rows_pad = (nrows + kWindow - 1) / kWindow * kWindow;
   int k = -2;
   // column-split plans (m_pad > 0): virtual rows b * m_pad + i with i >= m_real are padding
   if (r < nrows && (m_pad == 0 || r % m_pad < m_real)) {
@@ -805,20 +836,23 @@ __global__ void __launch_bounds__(kWindow) k_sell_plan(const int *rp, int nrows,
   int rank = t;
   if (sort_rows) {
     rank = 0;
-    for (int j = 0; j < kWindow; ++j) {
+    for (int j = 0; j < WIN; ++j) {
       const int kj = key[j];
       rank += (kj > k) || (kj == k && j < t);
     }
   }
   skey[rank] = k;
-  // column-split plans store the real row i of virtual row b * m_pad + i
-  slice_row[blockIdx.x * kWindow + rank] = k >= 0 ? (m_pad ? r % m_pad : r) : -1;
-  slice_len[blockIdx.x * kWindow + rank] = (unsigned short)(k >= 0 ? k : 0);
+  const int p = blockIdx.x * WIN + rank;
+  if (p < rows_pad) {
+    // column-split plans store the real row i of virtual row b * m_pad + i
+    slice_row[p] = k >= 0 ? (m_pad ? r % m_pad : r) : -1;
+    slice_len[p] = (unsigned short)(k >= 0 ? k : 0);
+  }
   __syncthreads();
-  if (t < kWindow / kSlice) {
+  if (t < WIN / kSlice && blockIdx.x * WIN + t * kSlice < rows_pad) {
     int mx = 0;
     for (int i = 0; i < kSlice; ++i) mx = max(mx, skey[t * kSlice + i]);
-    slice_slots[blockIdx.x * (kWindow / kSlice) + t] = mx * kSlice;
+    slice_slots[blockIdx.x * (WIN / kSlice) + t] = mx * kSlice;
   }
 }
 

@@ -221,11 +221,12 @@ struct RbRank {
   int64_t row0 = 0;          // first global row
 };
 
-// chunk geometry: K chunks of P slices of cw columns (cw a multiple of the SELL
-// window when K > 1, so a chunk is a whole number of SELL windows of A^T)
+// chunk geometry: K chunks of P slices of cw columns (cw a multiple of A^T's
+// SELL sorting window when K > 1, so a chunk is a whole number of windows)
 void rb_dims(int64_t n, int P, int K, int64_t *cw, int64_t *npad) {
   int64_t w = (n + (int64_t)K * P - 1) / ((int64_t)K * P);
-  if (K > 1) w = (w + kWindow - 1) / kWindow * kWindow;
+  const int win = sort_win(n);
+  if (K > 1) w = (w + win - 1) / win * win;
   *cw = std::max<int64_t>(w, 1);
   *npad = *cw * P * K;
 }

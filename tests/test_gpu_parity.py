@@ -107,6 +107,26 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert np.array_equal(dev.to_host("x"), st.x)
 
 
+@pytest.mark.parametrize("engine", ["sell", "split"])
+def test_iteration_bit_exact_midsize(engine, monkeypatch):
+    """140k x 140k, 7 per row: >= 131072 rows (the HPR_SORT_WIN threshold) and
+    the column-split A over seven 20k-column blocks."""
+    prob, _ = P.generate_planted_lp_fast(5, 70_000, 70_000, 140_000, 7)
+    _engine_env(monkeypatch, engine, prob.n)
+    dev = _dev(prob)
+    assert dev.layout_info()["split_a"] == (7 if engine == "split" else 0)
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.7, lam)
+    dev.state_reset()
+    dev.run_inner(12, 0, 0, 0.7, lam * 0.7, 2)
+    for _ in range(12):
+        O.iterate_once(st, slp)
+    assert np.array_equal(dev.to_host("y"), st.y)
+    assert np.array_equal(dev.to_host("x"), st.x)
+    dev.close()
+
+
 def test_scaling_and_power_vs_oracle():
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     dev = _dev(prob)
