@@ -197,6 +197,7 @@ typedef struct hpr_layout_info_t {
   int64_t slices_a, slices_at, slots_a, slots_at, long_rows_a, long_rows_at;
   int64_t cb_a, cb_at;   /* padded entries of the column-blocked layout (0: SELL engine) */
   int64_t split_a;       /* column blocks of A's split y-phase layout (0: not split) */
+  int64_t stg_a, stg_at; /* staged-engine vector chunks of A / A^T (0: engine off) */
 } hpr_layout_info_t;
 int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 

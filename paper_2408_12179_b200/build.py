@@ -10,6 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu"), os.path.join(HERE, "csrc", "hpr_mps.cpp")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
+              os.path.join(HERE, "csrc", "hpr_cb.cuh"),
+              os.path.join(HERE, "csrc", "hpr_stg.cuh"),
               os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
               os.path.join(HERE, "csrc", "hpr_batch.cuh"),
               os.path.join(ROOT, "include", "hprlp_b200.h")]

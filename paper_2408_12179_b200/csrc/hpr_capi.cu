@@ -19,6 +19,7 @@
 #include "../../include/hprlp_b200.h"
 #include "hpr_kernels.cuh"
 #include "hpr_cb.cuh"
+#include "hpr_stg.cuh"
 
 using namespace hpr;
 
@@ -142,7 +143,40 @@ SplitOff split_plan_of(const hpr_dims &d) {
   return o;
 }
 
+// STG engine (hpr_stg.cuh) for one matrix: rows x cols (cols = the staged
+// vector).  Auto when the vector is reused enough for streaming it through
+// every SM to beat gathering it (nnz >= 40 cols), the matrix is large enough
+// to fill the GPU, and it fits the engine's limits; HPR_STG=0 never, =1
+// whenever it fits.  The column-split and CB layouts take precedence.
+constexpr int kStgMaxG = 160;
+struct StgOff {
+  bool on = false;
+  int NB = 0;
+  int64_t items = 0;          // rows * NB
+  size_t row_start = 0, goff = 0;
+};
+// transpose: the matrix is A^T (x-phase).  HPR_STG=x / =y: force it for the
+// x-phase (A^T) / y-phase (A) only.
+StgOff stg_plan_of(int64_t rows, int64_t cols, int64_t nnz, bool transpose) {
+  StgOff o;
+  if (rows < 1 || cols < 1 || nnz < 1) return o;
+  const int64_t NB = (cols + kStgW - 1) / kStgW;
+  if (NB > 64 || rows * NB >= INT_MAX) return o;
+  const char *env = getenv("HPR_STG");
+  if (env && env[0] == '0') return o;
+  if (env && ((env[0] == 'x' && !transpose) || (env[0] == 'y' && transpose))) return o;
+  const bool forced = env && (env[0] == '1' || env[0] == 'x' || env[0] == 'y');
+  if (!forced && (nnz < 40 * cols || rows < 148 * 64)) return o;
+  o.on = true;
+  o.NB = (int)NB;
+  o.items = rows * NB;
+  return o;
+}
+
 struct Layout {
+  StgOff sa, sat;
+  size_t stg_key = 0, stg_lrow = 0, stg_skey = 0, stg_slrow = 0, stg_gstart = 0, stg_rbytes = 0,
+         stg_flag = 0;
   SplitOff sp;
   PlanOff pa, pat;
   CbOff ca, cat;
@@ -164,7 +198,18 @@ int cub_temp_bytes(const hpr_dims &d, size_t *bytes) {
   CK(cub::DeviceSelect::Flagged(nullptr, s3, cub::CountingInputIterator<int>(0),
                                 (const int *)nullptr, (int *)nullptr, (int *)nullptr,
                                 std::max<int64_t>(nmax, sp.V)));
-  *bytes = std::max(s1, std::max(s2, s3));
+  size_t s4 = 0, s5 = 0;
+  for (const StgOff &o : {stg_plan_of(d.m, d.n, d.nnz, false), stg_plan_of(d.n, d.m, d.nnz, true)}) {
+    if (!o.on) continue;
+    size_t a = 0, b = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned *)nullptr, (unsigned *)nullptr,
+                                       (const int *)nullptr, (int *)nullptr, (int)o.items, 0, 32));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b, (const long long *)nullptr, (long long *)nullptr,
+                                     (int)(kStgMaxG * o.NB + 1)));
+    s4 = std::max(s4, a);
+    s5 = std::max(s5, b);
+  }
+  *bytes = std::max(std::max(s1, std::max(s2, s3)), std::max(s4, s5));
   return HPR_OK;
 }
 
@@ -212,6 +257,26 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
   };
   L.ca = cbplan(d.m, d.n);
   L.cat = cbplan(d.n, d.m);
+  auto stgplan = [&](int64_t rows, int64_t cols, bool transpose) {
+    StgOff o = stg_plan_of(rows, cols, d.nnz, transpose);
+    if (!o.on) return o;
+    o.row_start = take(sizeof(int) * (kStgMaxG + 1));
+    o.goff = take(sizeof(long long) * ((size_t)kStgMaxG * o.NB + 1));
+    return o;
+  };
+  L.sa = L.ca.on ? StgOff{} : stgplan(d.m, d.n, false);
+  L.sat = L.cat.on ? StgOff{} : stgplan(d.n, d.m, true);
+  if (L.sa.on || L.sat.on) {
+    const int64_t it = std::max(L.sa.items, L.sat.items);
+    const int64_t ng = (int64_t)kStgMaxG * std::max(L.sa.NB, L.sat.NB) + 1;
+    L.stg_key = take(sizeof(unsigned) * it);
+    L.stg_lrow = take(sizeof(int) * it);
+    L.stg_skey = take(sizeof(unsigned) * it);
+    L.stg_slrow = take(sizeof(int) * it);
+    L.stg_gstart = take(sizeof(long long) * (ng + 1));
+    L.stg_rbytes = take(sizeof(long long) * (ng + 1));
+    L.stg_flag = take(sizeof(int));
+  }
   if (L.ca.on || L.cat.on) {
     L.cb_key = take(sizeof(int) * d.nnz);
     L.cb_lrow = take(sizeof(int) * d.nnz);
@@ -282,6 +347,14 @@ struct hpr_ctx {
     unsigned short *ci = nullptr;
     double *val = nullptr;
   } cba, cbat;
+  struct Stg {
+    bool on = false;
+    int G = 0, NB = 0, rows_cap = 0, rec_cap = 0, stages = 2, smem = 0;
+    long long rec_total = 0;
+    int *row_start = nullptr, *pos = nullptr;
+    long long *goff = nullptr;
+    unsigned char *rec = nullptr;
+  } sta, stat;
   int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
@@ -308,6 +381,9 @@ struct hpr_ctx {
   CbMat cbmat(const Cb &C, int ncols) const {
     return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
                  C.rows_cap, C.seg_cap, C.stages};
+  }
+  StgMat stgmat(const Stg &T, int ncols) const {
+    return StgMat{T.row_start, T.goff, T.rec, T.G, T.NB, ncols, T.rows_cap, T.rec_cap, T.stages};
   }
   SellMat mat_a(bool scaled) const {
     SellMat M = mat(sa, B.a_rp, B.a_ci, scaled ? B.a_val_s : B.a_val, scaled);
@@ -453,6 +529,115 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   if (total < 0) return fail(HPR_EINVAL, "SELL slot count overflows int32");
   S.slots = total;
   S.nlong = nl;
+  return HPR_OK;
+}
+
+// ---- STG engine: items, plan (hpr_analyze), layout (hpr_bind_layout) ----
+// (CTA, chunk, row) items of the rows, stably sorted by (CTA, chunk, count
+// desc); group starts into L.stg_gstart
+int stg_sort(hpr_ctx *c, const hpr_ctx::Stg &T, const int *rp, const int *ci, int rows) {
+  cudaStream_t s = c->stream;
+  const Layout &L = c->L;
+  unsigned *key = (unsigned *)(c->ws + L.stg_key), *skey = (unsigned *)(c->ws + L.stg_skey);
+  int *lrow = (int *)(c->ws + L.stg_lrow), *slrow = (int *)(c->ws + L.stg_slrow);
+  long long *gstart = (long long *)(c->ws + L.stg_gstart);
+  const long long items = (long long)rows * T.NB;
+  const int ng = T.G * T.NB;
+  k_stg_items<<<grid_for(rows), 256, 0, s>>>(rp, ci, rows, T.row_start, T.G, T.NB, key, lrow,
+                                             (int *)(c->ws + L.stg_flag));
+  CKL();
+  int end_bit = 17;
+  while ((1LL << (end_bit - 16)) < ng) ++end_bit;
+  size_t tb = L.cub_bytes;
+  CK(cub::DeviceRadixSort::SortPairs(c->ws + L.cub_tmp, tb, key, skey, lrow, slrow, (int)items, 0,
+                                     end_bit, s));
+  k_stg_gstart<<<grid_for(items), 256, 0, s>>>(skey, items, ng, gstart);
+  CKL();
+  c->launches += 3;
+  return HPR_OK;
+}
+
+int stg_plan(hpr_ctx *c, const StgOff &o, const int *rp, const int *ci, int rows,
+             hpr_ctx::Stg &T) {
+  T = hpr_ctx::Stg{};
+  if (!o.on || c->d.nnz == 0 || c->num_sms > kStgMaxG) return HPR_OK;
+  cudaStream_t s = c->stream;
+  const Layout &L = c->L;
+  T.G = std::min(c->num_sms, rows);
+  T.NB = o.NB;
+  T.row_start = (int *)(c->ws + o.row_start);
+  T.goff = (long long *)(c->ws + o.goff);
+  k_cb_rowstart<<<1, 1, 0, s>>>(rp, rows, T.G, T.row_start);
+  CKL();
+  CK(cudaMemsetAsync(c->ws + L.stg_flag, 0, sizeof(int), s));
+  c->launches += 1;
+  int rc = stg_sort(c, T, rp, ci, rows);
+  if (rc) return rc;
+  const int ng = T.G * T.NB;
+  long long *rbytes = (long long *)(c->ws + L.stg_rbytes);
+  k_stg_recsize<<<(ng + 127) / 128, 128, 0, s>>>((unsigned *)(c->ws + L.stg_skey),
+                                                 (long long *)(c->ws + L.stg_gstart), ng, rbytes);
+  CKL();
+  CK(cudaMemsetAsync(rbytes + ng, 0, sizeof(long long), s));
+  size_t tb = L.cub_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(c->ws + L.cub_tmp, tb, rbytes, T.goff, ng + 1, s));
+  c->launches += 2;
+  std::vector<int> hrs(T.G + 1);
+  std::vector<long long> hgo(ng + 1);
+  int flag = 0;
+  CK(cudaMemcpyAsync(hrs.data(), T.row_start, sizeof(int) * (T.G + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hgo.data(), T.goff, sizeof(long long) * (ng + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&flag, c->ws + L.stg_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int g = 0; g < T.G; ++g) T.rows_cap = std::max(T.rows_cap, hrs[g + 1] - hrs[g]);
+  long long rc_max = 0;
+  for (int q = 0; q < ng; ++q) rc_max = std::max(rc_max, hgo[q + 1] - hgo[q]);
+  T.rec_total = hgo[ng];
+  T.rec_cap = (int)std::min<long long>(rc_max, INT_MAX / 2);
+  T.stages = kStgMaxStages;
+  while (T.stages > 2 && stg_smem_bytes(T.stages, T.rows_cap, T.rec_cap) > kCbMaxSmem) --T.stages;
+  T.smem = stg_smem_bytes(T.stages, T.rows_cap, T.rec_cap);
+  T.on = !flag && rc_max <= kCbMaxSmem && T.smem <= kCbMaxSmem && T.rows_cap < (int)kStgPad &&
+         T.rec_total / 8 < INT_MAX;
+  return HPR_OK;
+}
+
+size_t stg_bytes(const hpr_ctx::Stg &T, int64_t nnz) {
+  if (!T.on) return 0;
+  return align_up((size_t)T.rec_total + 256, 256) + align_up((size_t)nnz * 4 + 256, 256);
+}
+
+int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *ci, int rows) {
+  if (!T.on) return HPR_OK;
+  cudaStream_t s = c->stream;
+  const long long nnz = c->d.nnz;
+  T.rec = (unsigned char *)p;
+  p += align_up((size_t)T.rec_total + 256, 256);
+  T.pos = (int *)p;
+  p += align_up((size_t)nnz * 4 + 256, 256);
+  CK(cudaMemsetAsync(T.rec, 0, (size_t)T.rec_total, s));
+  int rc = stg_sort(c, T, rp, ci, rows);
+  if (rc) return rc;
+  const int ng = T.G * T.NB;
+  const size_t sh = sizeof(int) * ((size_t)T.rows_cap / 32 + 3);
+  k_stg_fill<<<ng, 256, sh, s>>>(rp, ci, T.row_start, T.NB, (unsigned *)(c->ws + c->L.stg_skey),
+                                 (int *)(c->ws + c->L.stg_slrow),
+                                 (long long *)(c->ws + c->L.stg_gstart), T.goff, T.rec, T.pos);
+  CKL();
+  c->launches += 1;
+  return HPR_OK;
+}
+
+template <class Epi>
+int launch_stg(hpr_ctx *c, const hpr_ctx::Stg &T, int ncols, const double *xg, const Epi &epi) {
+  static bool smem_set = false;
+  if (!smem_set) {
+    CK(cudaFuncSetAttribute(k_stg<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
+    smem_set = true;
+  }
+  k_stg<Epi><<<T.G, kStgThreads, T.smem, c->stream>>>(c->stgmat(T, ncols), xg, epi);
+  CKL();
+  c->launches += 1;
   return HPR_OK;
 }
 
@@ -903,8 +1088,13 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   if (rc) return rc;
   rc = split_plan(c);
   if (rc) return rc;
+  rc = stg_plan(c, c->L.sa, B.a_rp, B.a_ci, m, c->sta);
+  if (rc) return rc;
+  rc = stg_plan(c, c->L.sat, B.at_rp, B.at_ci, n, c->stat);
+  if (rc) return rc;
   *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz) +
-                  cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz) + split_bytes(c->sp, d.nnz);
+                  cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz) + split_bytes(c->sp, d.nnz) +
+                  stg_bytes(c->sta, d.nnz) + stg_bytes(c->stat, d.nnz);
   c->analyzed = true;
   c->laid_out = false;
   return HPR_OK;
@@ -917,7 +1107,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (!layout) return fail(HPR_EINVAL, "null layout");
   if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz) +
                   cb_bytes(c->cba, c->d.nnz) + cb_bytes(c->cbat, c->d.nnz) +
-                  split_bytes(c->sp, c->d.nnz))
+                  split_bytes(c->sp, c->d.nnz) + stg_bytes(c->sta, c->d.nnz) +
+                  stg_bytes(c->stat, c->d.nnz))
     return fail(HPR_EINVAL, "layout buffer too small");
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
@@ -932,6 +1123,10 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (rc) return rc;
   rc = split_layout(c, p);
   if (rc) return rc;
+  rc = stg_layout(c, p, c->sta, B.a_rp, B.a_ci, (int)c->d.m);
+  if (rc) return rc;
+  rc = stg_layout(c, p, c->stat, B.at_rp, B.at_ci, (int)c->d.n);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(c->stream));
   // the captured graphs hold the layout's pointers and the plans' counts: keep
   // them when a re-analysed problem reproduces both (a re-solve of the same
@@ -940,6 +1135,10 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   for (const Sell *S : {&c->sa, &c->sat, &c->sp.S})
     for (long long v : {(long long)S->nslices, S->slots, (long long)S->nlong}) sig.push_back(v);
   for (long long v : {(long long)c->sp.on, (long long)c->sp.NB, (long long)c->sp.W}) sig.push_back(v);
+  for (const hpr_ctx::Stg *T : {&c->sta, &c->stat})
+    for (long long v : {(long long)T->on, (long long)T->G, (long long)T->NB, (long long)T->rows_cap,
+                        (long long)T->rec_cap, T->rec_total, (long long)T->stages})
+      sig.push_back(v);
   for (const hpr_ctx::Cb *C : {&c->cba, &c->cbat})
     for (long long v : {(long long)C->on, (long long)C->G, (long long)C->NB, (long long)C->rows_cap,
                         (long long)C->seg_cap, (long long)C->stages, C->npad, C->nrpb})
@@ -1040,6 +1239,11 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
     if (c->sp.on) k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sp.S.pos, B.a_val_s, c->sp.S.val_s, nnz);
     CKL();
     c->launches += 3 + (int)c->sp.on;
+    if (c->sta.on)
+      k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->sta.pos, B.a_val_s, (double *)c->sta.rec, nnz);
+    if (c->stat.on)
+      k_sell_scatter<<<grid_for(nnz), 256, 0, s>>>(c->stat.pos, B.at_val_s, (double *)c->stat.rec, nnz);
+    c->launches += (int)c->sta.on + (int)c->stat.on;
     if (c->cba.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cba.pos, B.a_val_s, c->cba.val, nnz);
     if (c->cbat.on) k_cb_scatter<<<grid_for(nnz), 256, 0, s>>>(c->cbat.pos, B.at_val_s, c->cbat.val, nnz);
     CKL();
@@ -1245,11 +1449,13 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
       ex.step = i;
       ey.step = i;
       // the first kernel of the graph follows the k_set_params launch: plain edge
-      int rc2 = c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
-                           : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
+      int rc2 = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
+                : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
+                             : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
       if (!rc2)
-        rc2 = c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
-                        : launch_a_iter(c, B.w, ey, true);
+        rc2 = c->sta.on ? launch_stg(c, c->sta, (int)c->d.n, B.w, ey)
+              : c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
+                          : launch_a_iter(c, B.w, ey, true);
       if (rc2) {
         cudaStreamEndCapture(s, &g);
         return rc2;
@@ -1411,6 +1617,8 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->cb_a = c->cba.on ? c->cba.npad : 0;
   info->cb_at = c->cbat.on ? c->cbat.npad : 0;
   info->split_a = c->sp.on ? c->sp.NB : 0;
+  info->stg_a = c->sta.on ? c->sta.NB : 0;
+  info->stg_at = c->stat.on ? c->stat.NB : 0;
   return HPR_OK;
 }
 

@@ -215,7 +215,8 @@ class RowBlockGroup:
     def layout_info(self) -> dict:
         infos = [b.layout_info() for b in self.blocks]
         out = {k: sum(i[k] for i in infos) for k in infos[0]}
-        out["split_a"] = max(i["split_a"] for i in infos)   # column blocks, not a count
+        for k in ("split_a", "stg_a", "stg_at"):       # column blocks / chunks, not counts
+            out[k] = max(i[k] for i in infos)
         out["partitions"] = self.P
         return out
 

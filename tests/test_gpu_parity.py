@@ -68,15 +68,18 @@ def assert_report_parity(rep, g, name=""):
 # ---------------------------------------------------------------------------
 
 # SELL-32-sigma / column-blocked smem-staged (HPR_CB) / SELL with A's columns
-# split into blocks whose running sums are carried block to block (HPR_SPLIT_COLS)
-ENGINES = ["sell", "cb", "split"]
+# split into blocks whose running sums are carried block to block
+# (HPR_SPLIT_COLS) / staged segmented engine (HPR_STG, both phases)
+ENGINES = ["sell", "cb", "split", "stg"]
 
 
 def _engine_env(monkeypatch, engine, n):
     monkeypatch.setenv("HPR_CB", "1" if engine == "cb" else "0")
+    monkeypatch.setenv("HPR_STG", "1" if engine == "stg" else "0")
     if engine == "split":
         monkeypatch.setenv("HPR_SPLIT_COLS", str(max(1, -(-n // 7))))   # 7 column blocks
     else:
+        monkeypatch.delenv("HPR_SPLIT_COLS", raising=False)
         monkeypatch.setenv("HPR_SPLIT", "0")
 
 
@@ -89,6 +92,7 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     info = dev.layout_info()
     assert (info["cb_a"] > 0 and info["cb_at"] > 0) == (engine == "cb")
     assert info["split_a"] == (7 if engine == "split" else 0)
+    assert (info["stg_a"] > 0 and info["stg_at"] > 0) == (engine == "stg")
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.83, lam,
@@ -107,14 +111,16 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert np.array_equal(dev.to_host("x"), st.x)
 
 
-@pytest.mark.parametrize("engine", ["sell", "split"])
+@pytest.mark.parametrize("engine", ["sell", "split", "stg"])
 def test_iteration_bit_exact_midsize(engine, monkeypatch):
     """140k x 140k, 7 per row: >= 131072 rows (the HPR_SORT_WIN threshold) and
     the column-split A over seven 20k-column blocks."""
     prob, _ = P.generate_planted_lp_fast(5, 70_000, 70_000, 140_000, 7)
     _engine_env(monkeypatch, engine, prob.n)
     dev = _dev(prob)
-    assert dev.layout_info()["split_a"] == (7 if engine == "split" else 0)
+    info = dev.layout_info()
+    assert info["split_a"] == (7 if engine == "split" else 0)
+    assert (info["stg_a"], info["stg_at"]) == ((18, 18) if engine == "stg" else (0, 0))
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.7, lam)
@@ -268,6 +274,26 @@ def test_c1_vs_reference(golden_reports):
     assert np.allclose(rep.solution.x, d["sol_x"], rtol=1e-8, atol=1e-10)
     assert np.allclose(rep.solution.y, d["sol_y"], rtol=1e-8, atol=1e-10)
     assert np.allclose(rep.solution.z, d["sol_z"], rtol=1e-8, atol=1e-10)
+
+
+def test_c2_engines_bit_identical(monkeypatch):
+    """C2: the staged engine (auto-selected for the x-phase) and SELL give the same bits."""
+    prob, _ = P.generate_known_solution_lp(2, 50_000, 50_000, 200_000, 2.5e-4)
+    out = {}
+    for stg in ("0", None):
+        if stg is None:
+            monkeypatch.delenv("HPR_STG", raising=False)
+        else:
+            monkeypatch.setenv("HPR_STG", stg)
+        dev = _dev(prob)
+        info = dev.layout_info()
+        assert (info["stg_a"], info["stg_at"]) == ((0, 0) if stg == "0" else (0, 13))
+        lam = dev.power(1e-4, 5000).raw * 1.001
+        dev.state_reset()
+        dev.run_inner(40, 0, 0, 0.9, lam * 0.9, 2)
+        out[stg] = (dev.to_host("y"), dev.to_host("x"))
+        dev.close()
+    assert np.array_equal(out["0"][0], out[None][0]) and np.array_equal(out["0"][1], out[None][1])
 
 
 def test_c2_vs_reference(golden_reports):
