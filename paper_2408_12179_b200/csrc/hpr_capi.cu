@@ -567,7 +567,7 @@ int stg_plan(hpr_ctx *c, const StgOff &o, const int *rp, const int *ci, int rows
   T.NB = o.NB;
   T.row_start = (int *)(c->ws + o.row_start);
   T.goff = (long long *)(c->ws + o.goff);
-  k_cb_rowstart<<<1, 1, 0, s>>>(rp, rows, T.G, T.row_start);
+  k_cb_rowstart<<<1, 256, 0, s>>>(rp, rows, T.G, T.row_start);
   CKL();
   CK(cudaMemsetAsync(c->ws + L.stg_flag, 0, sizeof(int), s));
   c->launches += 1;
@@ -630,10 +630,10 @@ int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *
 
 template <class Epi>
 int launch_stg(hpr_ctx *c, const hpr_ctx::Stg &T, int ncols, const double *xg, const Epi &epi) {
-  static bool smem_set = false;
-  if (!smem_set) {
-    CK(cudaFuncSetAttribute(k_stg<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
-    smem_set = true;
+  static int smem_set = 0;
+  if (T.smem > smem_set) {
+    CK(cudaFuncSetAttribute(k_stg<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, T.smem));
+    smem_set = T.smem;
   }
   k_stg<Epi><<<T.G, kStgThreads, T.smem, c->stream>>>(c->stgmat(T, ncols), xg, epi);
   CKL();
@@ -765,7 +765,7 @@ int cb_plan(hpr_ctx *c, const CbOff &o, const int *rp, const int *ci, int rows, 
   C.gstart = (int *)(c->ws + o.gstart);
   C.gseg = (long long *)(c->ws + o.gseg);
   C.rpb_base = (long long *)(c->ws + o.rpb_base);
-  k_cb_rowstart<<<1, 1, 0, s>>>(rp, rows, C.G, C.row_start);
+  k_cb_rowstart<<<1, 256, 0, s>>>(rp, rows, C.G, C.row_start);
   CKL();
   int rc = cb_sort(c, C, rp, ci);
   if (rc) return rc;

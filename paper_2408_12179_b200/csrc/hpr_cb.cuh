@@ -160,25 +160,32 @@ k_cb(CbMat M, const double *__restrict__ xg, Epi epi, double *part) {
 
 // ---- layout construction (hpr_analyze) ----
 // row_start[g] = first row whose prefix nnz reaches g * nnz / G (then forced
-// strictly increasing so every CTA owns at least one row)
+// strictly increasing so every CTA owns at least one row).  One block: thread
+// g binary-searches its boundary, thread 0 applies the monotone fix-up.
 __global__ void k_cb_rowstart(const int *rp, int nrows, int G, int *row_start) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const long long nnz = rp[nrows];
-  row_start[0] = 0;
-  int prev = 0;
-  for (int g = 1; g < G; ++g) {
+  for (int g = 1 + threadIdx.x; g < G; g += blockDim.x) {
     const long long target = (nnz * g) / G;
-    int lo = prev + 1, hi = nrows - (G - g);       // keep >= 1 row for the remaining CTAs
-    if (lo > hi) lo = hi;
-    int a = lo, z = hi;
+    int a = 0, z = nrows;
     while (a < z) {                                // first row r with rp[r] >= target
       const int mid = (a + z) >> 1;
       if ((long long)rp[mid] >= target) z = mid; else a = mid + 1;
     }
     row_start[g] = a;
-    prev = a;
   }
-  row_start[G] = nrows;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    row_start[0] = 0;
+    int prev = 0;
+    for (int g = 1; g < G; ++g) {
+      int a = row_start[g];
+      a = max(a, prev + 1);                        // >= 1 row for this CTA
+      a = min(a, nrows - (G - g));                 // >= 1 row for each later CTA
+      row_start[g] = a;
+      prev = a;
+    }
+    row_start[G] = nrows;
+  }
 }
 
 // key of every entry = g * NB + column block; local row of the entry
