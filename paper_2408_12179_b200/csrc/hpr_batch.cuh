@@ -85,12 +85,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+#ifndef HPR_BATCH_SROW
+#define HPR_BATCH_SROW 1   // 1: batches of 4 entries (loads in flight together, then the ordered adds)
+#endif
+
 // sequential sum of row r of a shared-memory CSR against vector v
 __device__ __forceinline__ double srow(const int *rp, const int *ci, const double *val,
                                        const double *v, int r) {
   double s = 0.0;
   int e = rp[r];
   const int e1 = rp[r + 1];
+#if HPR_BATCH_SROW
+  for (; e + 4 <= e1; e += 4) {
+    int c[4];
+    double a[4], x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = ci[e + u];
+      a[u] = val[e + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = v[c[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = __dadd_rn(s, __dmul_rn(a[u], x[u]));
+  }
+#endif
   for (; e < e1; ++e) s = __dadd_rn(s, __dmul_rn(val[e], v[ci[e]]));
   return s;
 }
@@ -103,6 +122,19 @@ __device__ __forceinline__ void srow2(const int *rp, const int *ci, const double
   s1 = 0.0;
   int e0 = rp[r0], e1 = r1 >= 0 ? rp[r1] : 0;
   const int z0 = rp[r0 + 1], z1 = r1 >= 0 ? rp[r1 + 1] : 0;
+#if HPR_BATCH_SROW
+  while (e0 + 2 <= z0 && e1 + 2 <= z1) {
+    const int c0 = ci[e0], c1 = ci[e0 + 1], d0 = ci[e1], d1 = ci[e1 + 1];
+    const double a0 = val[e0], a1 = val[e0 + 1], b0 = val[e1], b1 = val[e1 + 1];
+    const double x0 = v[c0], x1 = v[c1], y0 = v[d0], y1 = v[d1];
+    s0 = __dadd_rn(s0, __dmul_rn(a0, x0));
+    s1 = __dadd_rn(s1, __dmul_rn(b0, y0));
+    s0 = __dadd_rn(s0, __dmul_rn(a1, x1));
+    s1 = __dadd_rn(s1, __dmul_rn(b1, y1));
+    e0 += 2;
+    e1 += 2;
+  }
+#endif
   while (e0 < z0 && e1 < z1) {
     const double p0 = __dmul_rn(val[e0], v[ci[e0]]);
     const double p1 = __dmul_rn(val[e1], v[ci[e1]]);
