@@ -355,6 +355,7 @@ struct hpr_ctx {
     long long *goff = nullptr;
     unsigned char *rec = nullptr;
   } sta, stat;
+  const Stg *stg_sorted = nullptr;   // whose sorted items the STG temporaries hold
   int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
@@ -554,6 +555,7 @@ int stg_sort(hpr_ctx *c, const hpr_ctx::Stg &T, const int *rp, const int *ci, in
   k_stg_gstart<<<grid_for(items), 256, 0, s>>>(skey, items, ng, gstart);
   CKL();
   c->launches += 3;
+  c->stg_sorted = &T;
   return HPR_OK;
 }
 
@@ -616,8 +618,10 @@ int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *
   T.pos = (int *)p;
   p += align_up((size_t)nnz * 4 + 256, 256);
   CK(cudaMemsetAsync(T.rec, 0, (size_t)T.rec_total, s));
-  int rc = stg_sort(c, T, rp, ci, rows);
-  if (rc) return rc;
+  if (c->stg_sorted != &T) {          // hpr_analyze's sort of this matrix was overwritten
+    int rc = stg_sort(c, T, rp, ci, rows);
+    if (rc) return rc;
+  }
   const int ng = T.G * T.NB;
   const size_t sh = sizeof(int) * ((size_t)T.rows_cap / 32 + 3);
   k_stg_fill<<<ng, 256, sh, s>>>(rp, ci, T.row_start, T.NB, (unsigned *)(c->ws + c->L.stg_skey),
@@ -1088,6 +1092,7 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   if (rc) return rc;
   rc = split_plan(c);
   if (rc) return rc;
+  c->stg_sorted = nullptr;
   rc = stg_plan(c, c->L.sa, B.a_rp, B.a_ci, m, c->sta);
   if (rc) return rc;
   rc = stg_plan(c, c->L.sat, B.at_rp, B.at_ci, n, c->stat);
@@ -1363,7 +1368,14 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < kPowBatch; ++i) {
       int ga = 0;
-      rc = launch_sell(c, c->mat_at(true), v, et, P.powt, nullptr);
+      if (c->stat.on) {
+        EpiPowTu eu{};
+        eu.u = u;
+        eu.S = c->pow;
+        rc = launch_stg(c, c->stat, (int)c->d.m, v, eu);
+      } else {
+        rc = launch_sell(c, c->mat_at(true), v, et, P.powt, nullptr);
+      }
       if (!rc) rc = launch_sell(c, c->mat_a(true), u, ea, P.powa, &ga);
       if (rc) {
         cudaStreamEndCapture(s, &g);

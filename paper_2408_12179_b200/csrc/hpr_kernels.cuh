@@ -684,6 +684,16 @@ struct EpiPowT {
     acc[0] = __dadd_rn(acc[0], sq(s));
   }
 };
+// u = A^T v without the norm (the in-loop power step only uses EpiPowA's sums;
+// staged-engine eligible)
+struct EpiPowTu {
+  static constexpr int NQ = 0;
+  double *u;
+  const PowState *S;
+  __device__ bool enter() { return !S->done; }
+  __device__ void prefetch(int) {}
+  __device__ void finish(int j, double s, double *) { u[j] = s; }
+};
 struct EpiPowA {
   static constexpr int NQ = 2;
   const double *v;
