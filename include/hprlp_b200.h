@@ -201,6 +201,14 @@ typedef struct hpr_layout_info_t {
 } hpr_layout_info_t;
 int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 
+/* Plain sparse product on the bound problem's current (scaled) values:
+ * y = A x (transpose = 0, x: n, y: m) or y = A^T x (transpose = 1, x: m,
+ * y: n); each row summed left to right from 0.0 like scipy's csr_matvec.
+ * Replaces SparseMatrix.apply / t_apply (sparse.py:102-108) for the exact
+ * T1 = 0 path (exact.py:70-75, 94-103, 200-272); asynchronous on the
+ * context's stream.  Requires hpr_analyze + hpr_bind_layout + hpr_scale. */
+int hpr_spmv(hpr_ctx *ctx, int transpose, const double *x, double *y);
+
 /* Device time (ms) of the last hpr_run_inner and of the last checkpoint,
  * measured with CUDA events on the context stream. */
 int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);

@@ -11,6 +11,8 @@ from .driver import (KktResidual, RestartEvent, RestartKind, SolveReport, Solver
                      SolveStatus, Timings, Variant, check_restart, check_termination,
                      kkt_residual, sigma_guards_pass, solve)
 from .generators import generate_flow_lp, generate_known_solution_lp, generate_planted_lp_fast
+from .exact import (halpern_padmm_trace, hpr_no_prox_trace, max_trace_gap, solve_equality_exact,
+                    solve_normal_equations)
 from .mps import MpsParseError, load_mps, parse_mps, write_mps
 from .problem import (DimensionMismatchError, LpProblem, PrimalDualPoint, SparseMatrix,
                       dual_objective, primal_objective, project_onto_box,
@@ -23,7 +25,8 @@ __all__ = [
     "parse_mps", "write_mps", "PrimalDualPoint", "RestartEvent",
     "RestartKind", "SolveReport", "SolveStatus", "SolverConfig", "SparseMatrix", "Timings",
     "Variant", "check_restart", "check_termination", "dual_objective",
-    "generate_flow_lp", "generate_known_solution_lp", "generate_planted_lp_fast",
+    "generate_flow_lp", "halpern_padmm_trace", "hpr_no_prox_trace", "max_trace_gap",
+    "solve_equality_exact", "solve_normal_equations", "generate_known_solution_lp", "generate_planted_lp_fast",
     "kkt_residual", "primal_objective", "project_onto_box", "project_onto_dual_cone",
     "sigma_guards_pass", "solve",
 ]

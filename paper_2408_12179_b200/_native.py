@@ -144,6 +144,7 @@ _SIGS = {
                                     ctypes.POINTER(HprCkptOut)]),
     "hpr_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "hpr_layout_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprLayoutInfo)]),
+    "hpr_spmv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "hpr_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
     # row-block partitioned mode (hpr_rowblock.cuh)

@@ -1648,3 +1648,14 @@ int hpr_last_times(hpr_ctx *c, double *inner_ms, double *ckpt_ms) {
 
 #include "hpr_rowblock.cuh"
 #include "hpr_batch.cuh"
+
+extern "C" int hpr_spmv(hpr_ctx *c, int transpose, const double *x, double *y) {
+  int rc = check_ctx(c, true, true);
+  if (rc) return rc;
+  if (!x || !y) return fail(HPR_EINVAL, "null vector");
+  CK(cudaSetDevice(c->device));
+  EpiStore e{};
+  e.out = y;
+  e.S = nullptr;
+  return launch_sell(c, transpose ? c->mat_at(true) : c->mat_a(true), x, e, nullptr, nullptr);
+}

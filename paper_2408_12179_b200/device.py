@@ -289,6 +289,12 @@ class DeviceLP:
         N.call("hpr_kkt_origin", self.ctx, int(term_original), int(slot), ctypes.byref(out))
         return out
 
+    def spmv(self, transpose: bool, x, y):
+        """y = A x or A^T x on the current (scaled) values (device tensors,
+        the context's stream; hpr_spmv)."""
+        N.call("hpr_spmv", self.ctx, int(bool(transpose)), ctypes.c_void_p(x.data_ptr()),
+               ctypes.c_void_p(y.data_ptr()))
+
     def kkt(self, term_original, slot):
         out = N.HprCkptOut()
         N.call("hpr_kkt", self.ctx, int(term_original), int(slot), ctypes.byref(out))
