@@ -85,16 +85,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+#ifndef HPR_BATCH_PROF
+#define HPR_BATCH_PROF 0
+#endif
 #ifndef HPR_BATCH_SROW
 #define HPR_BATCH_SROW 1   // 1: batches of 4 entries (loads in flight together, then the ordered adds)
 #endif
 
-// sequential sum of row r of a shared-memory CSR against vector v
-__device__ __forceinline__ double srow(const int *rp, const int *ci, const double *val,
-                                       const double *v, int r) {
+// Shared-memory matrices are stored POSITION-MAJOR: rows sorted by length
+// (longest first, perm[p] = row at position p), row p's entries contiguous
+// from st[p] in ascending column order, every row padded to an odd length so
+// the 32 lanes of a warp (consecutive positions, equal lengths) hit distinct
+// shared-memory banks (the CSR layout put 4-way conflicts on every load).
+// Column indices are 16-bit (LPs of a batch have < 65536 rows and columns).
+typedef unsigned short u16;
+
+// sequential sum of the row at position p against vector v
+__device__ __forceinline__ double srow(const int *st, const u16 *ln, const u16 *ci,
+                                       const double *val, const double *v, int p) {
   double s = 0.0;
-  int e = rp[r];
-  const int e1 = rp[r + 1];
+  int e = st[p];
+  const int e1 = e + ln[p];
 #if HPR_BATCH_SROW
   for (; e + 4 <= e1; e += 4) {
     int c[4];
@@ -115,13 +126,14 @@ __device__ __forceinline__ double srow(const int *rp, const int *ci, const doubl
 }
 
 // two rows at once (independent chains interleaved: twice the shared-memory
-// loads in flight per thread); each row still summed left to right.  r1 < 0: none
-__device__ __forceinline__ void srow2(const int *rp, const int *ci, const double *val,
-                                      const double *v, int r0, int r1, double &s0, double &s1) {
+// loads in flight per thread); each row still summed left to right.  p1 < 0: none
+__device__ __forceinline__ void srow2(const int *st, const u16 *ln, const u16 *ci,
+                                      const double *val, const double *v, int p0, int p1,
+                                      double &s0, double &s1) {
   s0 = 0.0;
   s1 = 0.0;
-  int e0 = rp[r0], e1 = r1 >= 0 ? rp[r1] : 0;
-  const int z0 = rp[r0 + 1], z1 = r1 >= 0 ? rp[r1 + 1] : 0;
+  int e0 = st[p0], e1 = p1 >= 0 ? st[p1] : 0;
+  const int z0 = e0 + ln[p0], z1 = p1 >= 0 ? e1 + ln[p1] : 0;
 #if HPR_BATCH_SROW
   while (e0 + 2 <= z0 && e1 + 2 <= z1) {
     const int c0 = ci[e0], c1 = ci[e0 + 1], d0 = ci[e1], d1 = ci[e1 + 1];
@@ -136,10 +148,10 @@ __device__ __forceinline__ void srow2(const int *rp, const int *ci, const double
   }
 #endif
   while (e0 < z0 && e1 < z1) {
-    const double p0 = __dmul_rn(val[e0], v[ci[e0]]);
-    const double p1 = __dmul_rn(val[e1], v[ci[e1]]);
-    s0 = __dadd_rn(s0, p0);
-    s1 = __dadd_rn(s1, p1);
+    const double q0 = __dmul_rn(val[e0], v[ci[e0]]);
+    const double q1 = __dmul_rn(val[e1], v[ci[e1]]);
+    s0 = __dadd_rn(s0, q0);
+    s1 = __dadd_rn(s1, q1);
     ++e0;
     ++e1;
   }
@@ -158,11 +170,13 @@ __device__ __forceinline__ double grow(const int *rp, int base, const int *ci, c
 }
 
 size_t smem_bytes(int m, int n, long long nnz) {
+  const size_t slots = 2 * (size_t)nnz + m + n;  // A and A^T, rows padded to odd lengths
   size_t b = 0;
-  b += 2 * (size_t)nnz * 8;                    // av, atv
+  b += slots * 8;                              // av, atv
   b += 8 * (size_t)(5 * m + 8 * n);            // y ay bs yb rs | x ax w cs ls us csc xb
-  b += 2 * (size_t)nnz * 4;                    // aci, atci
-  b += 4 * (size_t)(m + 1 + n + 1);            // arp, atrp
+  b += 4 * (size_t)(m + n);                    // ast, atst (row starts by position)
+  b += slots * 2;                              // aci, atci (16-bit)
+  b += 2 * (size_t)(m + n) * 2;                // alen, atlen, aperm, atperm
   b = (b + 15) / 16 * 16;
   b += 8 * (size_t)24 * kBW;                   // reduction scratch
   b += 16 * (size_t)kWTab;                     // Halpern weight table
@@ -173,14 +187,17 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lp = blockIdx.x, tid = threadIdx.x;
   const unsigned long long t_start = gtimer();
+#if HPR_BATCH_PROF
+  const long long tk0 = clock64();
+#endif
   const long long r0 = P.row_off[lp], c0 = P.col_off[lp], z0 = P.nz_off[lp];
   const int m = (int)(P.row_off[lp + 1] - r0), n = (int)(P.col_off[lp + 1] - c0);
   const int nnz = (int)(P.nz_off[lp + 1] - z0);
   const int m1 = P.m1[lp];
   // ---- carve shared memory ----
   double *p = (double *)smraw;
-  double *av = p; p += nnz;
-  double *atv = p; p += nnz;
+  double *av = p; p += nnz + m;
+  double *atv = p; p += nnz + n;
   double *y = p; p += m;
   double *ay = p; p += m;
   double *bs = p; p += m;
@@ -194,12 +211,15 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   double *us = p; p += n;
   double *csc = p; p += n;
   double *xb = p; p += n;
-  int *ip = (int *)p;
-  int *aci = ip; ip += nnz;
-  int *atci = ip; ip += nnz;
-  int *arp = ip; ip += m + 1;
-  int *atrp = ip; ip += n + 1;
-  double *red = (double *)(((uintptr_t)ip + 15) & ~(uintptr_t)15);
+  int *ast = (int *)p;
+  int *atst = ast + m;
+  u16 *aci = (u16 *)(atst + n);
+  u16 *atci = aci + nnz + m;
+  u16 *alen = atci + nnz + n;
+  u16 *atlen = alen + m;
+  u16 *aperm = atlen + n;
+  u16 *atperm = aperm + m;
+  double *red = (double *)(((uintptr_t)(atperm + n) + 15) & ~(uintptr_t)15);
   double *wtab = red + 24 * kBW;
   // global views of this LP
   const int *grp = P.rp + r0 + lp;             // local row pointers (m + 1)
@@ -212,14 +232,65 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   double *ox = O.x + c0, *oy = O.y + r0, *oz = O.z + c0, *gdy = O.dy + r0;
   const int tz = (int)z0;
 
-  for (int e = tid; e < nnz; e += kBT) {
-    aci[e] = gci[e];
-    av[e] = gval[e];
-    atci[e] = gtci[e];
-    atv[e] = gtval[e];
+  // ---- position-major shared-memory copies of A and A^T ----
+  // ranks by (length desc, index asc)
+  for (int i = tid; i < m; i += kBT) {
+    const int li = grp[i + 1] - grp[i];
+    int rank = 0;
+    for (int q = 0; q < m; ++q) {
+      const int lq = grp[q + 1] - grp[q];
+      rank += (lq > li) || (lq == li && q < i);
+    }
+    aperm[rank] = (u16)i;
+    alen[rank] = (u16)li;
   }
-  for (int i = tid; i <= m; i += kBT) arp[i] = grp[i];
-  for (int j = tid; j <= n; j += kBT) atrp[j] = gtrp[j] - tz;
+  for (int j = tid; j < n; j += kBT) {
+    const int lj = gtrp[j + 1] - gtrp[j];
+    int rank = 0;
+    for (int q = 0; q < n; ++q) {
+      const int lq = gtrp[q + 1] - gtrp[q];
+      rank += (lq > lj) || (lq == lj && q < j);
+    }
+    atperm[rank] = (u16)j;
+    atlen[rank] = (u16)lj;
+  }
+  __syncthreads();
+  if (tid == 0) {                                // row starts, every row padded to odd length
+    int o = 0;
+    for (int q = 0; q < m; ++q) {
+      ast[q] = o;
+      o += alen[q] | 1;
+    }
+  } else if (tid == 32) {
+    int o = 0;
+    for (int q = 0; q < n; ++q) {
+      atst[q] = o;
+      o += atlen[q] | 1;
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < m; q += kBT) {
+    const int i = aperm[q], g0 = grp[i], L = alen[q], o = ast[q];
+    for (int k2 = 0; k2 < L; ++k2) {
+      av[o + k2] = gval[g0 + k2];
+      aci[o + k2] = (u16)gci[g0 + k2];
+    }
+    if (!(L & 1)) {
+      av[o + L] = 0.0;
+      aci[o + L] = 0;
+    }
+  }
+  for (int q = tid; q < n; q += kBT) {
+    const int j = atperm[q], g0 = gtrp[j] - tz, L = atlen[q], o = atst[q];
+    for (int k2 = 0; k2 < L; ++k2) {
+      atv[o + k2] = gtval[g0 + k2];
+      atci[o + k2] = (u16)gtci[g0 + k2];
+    }
+    if (!(L & 1)) {
+      atv[o + L] = 0.0;
+      atci[o + L] = 0;
+    }
+  }
   for (int i = tid; i < m; i += kBT) rs[i] = 1.0;
   for (int j = tid; j < n; j += kBT) csc[j] = 1.0;
   __syncthreads();
@@ -227,48 +298,51 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   // ---- scale_problem (scaling.py:81-103) ----
   // one pass: row divisors in yb, column divisors in xb, then both value copies
   // become (v / dr[row]) / dc[col]
+  // (loops run over positions q: row aperm[q] / column atperm[q])
   auto apply_pass = [&]() {
-    for (int i = tid; i < m; i += kBT) {
+    for (int q = tid; q < m; q += kBT) {
+      const int i = aperm[q];
       const double d = yb[i];
       rs[i] = __dmul_rn(rs[i], d);
-      for (int e = arp[i]; e < arp[i + 1]; ++e) av[e] = __ddiv_rn(__ddiv_rn(av[e], d), xb[aci[e]]);
+      for (int e = ast[q]; e < ast[q] + alen[q]; ++e) av[e] = __ddiv_rn(__ddiv_rn(av[e], d), xb[aci[e]]);
     }
-    for (int j = tid; j < n; j += kBT) {
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
       const double d = xb[j];
       csc[j] = __dmul_rn(csc[j], d);
-      for (int e = atrp[j]; e < atrp[j + 1]; ++e)
+      for (int e = atst[q]; e < atst[q] + atlen[q]; ++e)
         atv[e] = __ddiv_rn(__ddiv_rn(atv[e], yb[atci[e]]), d);
     }
     __syncthreads();
   };
   for (int it = 0; it < C.ruiz; ++it) {
-    for (int i = tid; i < m; i += kBT) {
+    for (int q = tid; q < m; q += kBT) {
       double mx = 0.0;
-      for (int e = arp[i]; e < arp[i + 1]; ++e) mx = fmax(mx, fabs(av[e]));
+      for (int e = ast[q]; e < ast[q] + alen[q]; ++e) mx = fmax(mx, fabs(av[e]));
       double d = sqrt(mx);
-      yb[i] = d == 0.0 ? 1.0 : d;
+      yb[aperm[q]] = d == 0.0 ? 1.0 : d;
     }
-    for (int j = tid; j < n; j += kBT) {
+    for (int q = tid; q < n; q += kBT) {
       double mx = 0.0;
-      for (int e = atrp[j]; e < atrp[j + 1]; ++e) mx = fmax(mx, fabs(atv[e]));
+      for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) mx = fmax(mx, fabs(atv[e]));
       double d = sqrt(mx);
-      xb[j] = d == 0.0 ? 1.0 : d;
+      xb[atperm[q]] = d == 0.0 ? 1.0 : d;
     }
     __syncthreads();
     apply_pass();
   }
   if (C.pc) {
-    for (int i = tid; i < m; i += kBT) {
+    for (int q = tid; q < m; q += kBT) {
       double s = 0.0;
-      for (int e = arp[i]; e < arp[i + 1]; ++e) s = __dadd_rn(s, fabs(av[e]));
+      for (int e = ast[q]; e < ast[q] + alen[q]; ++e) s = __dadd_rn(s, fabs(av[e]));
       double d = sqrt(s);
-      yb[i] = d == 0.0 ? 1.0 : d;
+      yb[aperm[q]] = d == 0.0 ? 1.0 : d;
     }
-    for (int j = tid; j < n; j += kBT) {
+    for (int q = tid; q < n; q += kBT) {
       double s = 0.0;
-      for (int e = atrp[j]; e < atrp[j + 1]; ++e) s = __dadd_rn(s, fabs(atv[e]));
+      for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) s = __dadd_rn(s, fabs(atv[e]));
       double d = sqrt(s);
-      xb[j] = d == 0.0 ? 1.0 : d;
+      xb[atperm[q]] = d == 0.0 ? 1.0 : d;
     }
     __syncthreads();
     apply_pass();
@@ -307,13 +381,16 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     cnorm = sqrt(v2[1]);
   }
 
+#if HPR_BATCH_PROF
+  long long tp_setup = clock64(), tp_pow = 0, tp_it = 0, tp_ck = 0;
+#endif
   // ---- power method (sparse.py:165-203): v in yb, u in w, A u in ay ----
   int start = -2;
   for (int fb = -1; fb < m; ++fb) {
     for (int i = tid; i < m; i += kBT) yb[i] = fb < 0 ? 1.0 : (i == fb ? 1.0 : 0.0);
     __syncthreads();
     double u2[1] = {0.0};
-    for (int j = tid; j < n; j += kBT) u2[0] = __dadd_rn(u2[0], sq(srow(atrp, atci, atv, yb, j)));
+    for (int q = tid; q < n; q += kBT) u2[0] = __dadd_rn(u2[0], sq(srow(atst, atlen, atci, atv, yb, q)));
     bsum<1>(u2, red);
     if (sqrt(u2[0]) > 0.0) {
       start = fb;
@@ -330,11 +407,12 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   if (start != -2) {
     for (int it = 1; it <= C.power_max; ++it) {
       piters = it;
-      for (int j = tid; j < n; j += kBT) w[j] = srow(atrp, atci, atv, yb, j);
+      for (int q = tid; q < n; q += kBT) w[atperm[q]] = srow(atst, atlen, atci, atv, yb, q);
       __syncthreads();
       double d2[2] = {0.0, 0.0};
-      for (int i = tid; i < m; i += kBT) {
-        const double s = srow(arp, aci, av, w, i);
+      for (int q = tid; q < m; q += kBT) {
+        const int i = aperm[q];
+        const double s = srow(ast, alen, aci, av, w, q);
         ay[i] = s;
         d2[0] = __dadd_rn(d2[0], __dmul_rn(yb[i], s));
         d2[1] = __dadd_rn(d2[1], sq(s));
@@ -373,8 +451,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   // KKT terms of the candidate in (oy, oz, ox) on the termination problem;
   // results into kk[] (driver.py:203-216)
   auto kkt = [&](double (&s)[11]) {
-    for (int i = tid; i < m; i += kBT) {
-      const double axi = term_orig ? grow(grp, 0, gci, gval, ox, i) : srow(arp, aci, av, ox, i);
+    for (int q = tid; q < m; q += kBT) {
+      const int i = aperm[q];
+      const double axi = term_orig ? grow(grp, 0, gci, gval, ox, i) : srow(ast, alen, aci, av, ox, q);
       const double bi = term_orig ? b0[i] : bs[i];
       const double yi = oy[i];
       double prim = __dsub_rn(bi, axi);
@@ -387,8 +466,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       s[1] = __dadd_rn(s[1], __dmul_rn(bi, yi));
       s[2] = __dadd_rn(s[2], sq(__dsub_rn(yi, tproj)));
     }
-    for (int j = tid; j < n; j += kBT) {
-      const double aty = term_orig ? grow(gtrp, tz, gtci, gtval, oy, j) : srow(atrp, atci, atv, oy, j);
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
+      const double aty = term_orig ? grow(gtrp, tz, gtci, gtval, oy, j) : srow(atst, atlen, atci, atv, oy, q);
       const double cj = term_orig ? c0v[j] : cs[j];
       const double l = term_orig ? l0[j] : ls[j];
       const double u = term_orig ? u0[j] : us[j];
@@ -433,7 +513,13 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     clamped = (long long)s[9];
   };
 
+#if HPR_BATCH_PROF
+  tp_pow = clock64();
+#endif
   while (status < 0) {
+#if HPR_BATCH_PROF
+    const long long tq0 = clock64();
+#endif
     const long long steps = C.max_iter - k < C.check_interval ? C.max_iter - k : C.check_interval;
     const double lamsig = lamv * sigma;
     bool broke = false;
@@ -450,10 +536,12 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       }
       const double wn = wtab[2 * (st % kWTab)], wa = wtab[2 * (st % kWTab) + 1];
       int bad = 0;
-      for (int j = tid; j < n; j += 2 * kBT) {   // x phase (core.py:168-169), 2 columns
-        const int j2 = j + kBT < n ? j + kBT : -1;
+      for (int q = tid; q < n; q += 2 * kBT) {   // x phase (core.py:168-169), 2 columns
+        const int j = atperm[q];
+        const int q2 = q + kBT < n ? q + kBT : -1;
+        const int j2 = q2 >= 0 ? atperm[q2] : -1;
         double aty0, aty1;
-        srow2(atrp, atci, atv, y, j, j2, aty0, aty1);
+        srow2(atst, atlen, atci, atv, y, q, q2, aty0, aty1);
         for (int h = 0; h < 2; ++h) {
         const int jj = h ? j2 : j;
         if (jj < 0) break;
@@ -471,8 +559,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
         }
       }
       __syncthreads();
-      for (int i = tid; i < m; i += kBT) {       // y phase (core.py:170-172)
-        const double s = srow(arp, aci, av, w, i);
+      for (int q = tid; q < m; q += kBT) {       // y phase (core.py:170-172)
+        const int i = aperm[q];
+        const double s = srow(ast, alen, aci, av, w, q);
         const double yi = y[i];
         double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
         if (i >= m1) ybi = np_max(ybi, 0.0);
@@ -491,6 +580,10 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       ++t;
       ++k;
     }
+#if HPR_BATCH_PROF
+    const long long tq1 = clock64();
+    tp_it += tq1 - tq0;
+#endif
     if (broke) {
       status = 3;
       break;
@@ -499,8 +592,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     double s17[17];
 #pragma unroll
     for (int q = 0; q < 17; ++q) s17[q] = 0.0;
-    for (int j = tid; j < n; j += kBT) {
-      const double aty = srow(atrp, atci, atv, y, j);
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
+      const double aty = srow(atst, atlen, atci, atv, y, q);
       const double xj = x[j];
       const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
       const double xbj = np_clip(v, ls[j], us[j]);
@@ -519,8 +613,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       }
     }
     __syncthreads();
-    for (int i = tid; i < m; i += kBT) {
-      const double s = srow(arp, aci, av, w, i);
+    for (int q = tid; q < m; q += kBT) {
+      const int i = aperm[q];
+      const double s = srow(ast, alen, aci, av, w, q);
       const double yi = y[i];
       double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
       if (i >= m1) ybi = np_max(ybi, 0.0);
@@ -533,9 +628,10 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     }
     __syncthreads();
     // merit terms (core.py:191-197): A^T dy
-    for (int j = tid; j < n; j += kBT) {
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
       double a = 0.0;
-      for (int e = atrp[j]; e < atrp[j + 1]; ++e) a = __dadd_rn(a, __dmul_rn(atv[e], gdy[atci[e]]));
+      for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) a = __dadd_rn(a, __dmul_rn(atv[e], gdy[atci[e]]));
       const double dx = __dsub_rn(x[j], xb[j]);
       s17[4] = __dadd_rn(s17[4], sq(__dadd_rn(dx, __dmul_rn(sigma, a))));   // sh2
       s17[5] = __dadd_rn(s17[5], sq(a));                                    // aty2
@@ -677,6 +773,11 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     R.b_factor = bf;
     R.c_factor = cf;
     R.device_seconds = (double)(gtimer() - t_start) * 1e-9;
+#if HPR_BATCH_PROF
+    if (lp < 3)
+      printf("batch prof lp=%d setup+scale=%lld power=%lld iterations=%lld (%lld its) rest=%lld cycles\n", lp,
+             tp_setup - tk0, tp_pow - tp_setup, tp_it, (long long)k, clock64() - tp_pow - tp_it);
+#endif
   }
 }
 
@@ -785,6 +886,8 @@ int hpr_batch_solve(const hpr_batch_problem *p, const hpr_batch_config *cfg, voi
   int rc = batch_layout(p, &L);
   if (rc) return rc;
   if (ws_bytes < L.total) return fail(HPR_EINVAL, "batch workspace too small");
+  if (p->max_m > 65535 || p->max_n > 65535)
+    return fail(HPR_EINVAL, "an LP of the batch exceeds 65535 rows or columns");
   const size_t smem = smem_bytes(p->max_m, p->max_n, p->max_nnz);
   int dev_smem = 0;
   CK(cudaSetDevice(device));
