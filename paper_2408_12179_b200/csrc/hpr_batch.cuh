@@ -26,7 +26,10 @@
 namespace hpr {
 namespace batch {
 
-constexpr int kBT = 512;            // threads per CTA (one LP)
+#ifndef HPR_BATCH_THREADS
+#define HPR_BATCH_THREADS 512
+#endif
+constexpr int kBT = HPR_BATCH_THREADS;   // threads per CTA (one LP)
 constexpr int kWTab = 256;          // Halpern weights tabulated per refill
 constexpr int kBW = kBT / 32;
 
