@@ -190,43 +190,53 @@ class BatchRun:
 
     def reports(self, cfg: SolverConfig) -> list[SolveReport]:
         self.stream.synchronize()
-        pk = self.packed
-        raw = self.res.cpu().numpy().tobytes()
-        lraw = self.log.cpu().numpy().tobytes()
-        x, y, z = self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy()
-        rs = (N.HprBatchResult * pk.count).from_buffer_copy(raw)
-        recs = (N.HprRestartRec * (pk.count * MAX_LOG)).from_buffer_copy(lraw)
-        out = []
-        for i in range(pk.count):
-            r = rs[i]
-            if r.power_iterations and not r.power_converged:
-                warnings.warn(f"power method did not converge within {r.power_iterations} "
-                              "iterations", RuntimeWarning)
-            if r.merit_negative:
-                warnings.warn("negative quadratic form in the merit: lambda may underestimate "
-                              "lambda_1(AA*)", RuntimeWarning)
-            k = list(r.kkt)
-            kkt = KktResidual(k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8],
-                              int(r.dual_clamped))
-            log = []
-            for q in range(min(r.n_log, MAX_LOG)):
-                e = recs[i * MAX_LOG + q]
-                log.append(RestartEvent(int(e.outer_index), _TRIGGER[int(e.trigger)], int(e.tau),
-                                        float(e.sigma_next), float(e.merit)))
-            c0, c1 = int(pk.col_off[i]), int(pk.col_off[i + 1])
-            r0, r1 = int(pk.row_off[i]), int(pk.row_off[i + 1])
-            sol = PrimalDualPoint(y=y[r0:r1].copy(), z=z[c0:c1].copy(), x=x[c0:c1].copy())
-            tm = Timings(iteration_seconds=float(r.device_seconds))
-            out.append(SolveReport(
-                status=_STATUS[int(r.status)], primal_objective=float(r.primal_objective),
-                dual_objective=float(r.dual_objective), kkt=kkt, iterations=int(r.iterations),
-                restarts=int(r.restarts), restart_log=log, timings=tm, solution=sol,
-                sigma_final=float(r.sigma_final), lambda_estimate=float(r.lambda_estimate),
-                device_stats={"lambda_raw": float(r.lambda_raw),
-                              "power_iterations": int(r.power_iterations),
-                              "b_factor": float(r.b_factor), "c_factor": float(r.c_factor),
-                              "batch_index": i}))
-        return out
+        return _build_reports(self.packed, self.res.cpu().numpy(), self.log.cpu().numpy(),
+                              self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy())
+
+
+def _build_reports(pk: PackedBatch, raw, lraw, x, y, z) -> list[SolveReport]:
+    """SolveReports of a batch from the device result records (column-wise
+    numpy views of the C structs; the solution arrays are views of fresh host
+    copies of the batch vectors)."""
+    rs = np.frombuffer(np.ascontiguousarray(raw).tobytes(), dtype=np.dtype(N.HprBatchResult),
+                       count=pk.count)
+    recs = np.frombuffer(np.ascontiguousarray(lraw).tobytes(), dtype=np.dtype(N.HprRestartRec),
+                         count=pk.count * MAX_LOG).reshape(pk.count, MAX_LOG)
+    col = {f: rs[f].tolist() for f in rs.dtype.names if f != "kkt"}
+    kkts = rs["kkt"].tolist()
+    if any(p and not c for p, c in zip(col["power_iterations"], col["power_converged"])):
+        for p, c in zip(col["power_iterations"], col["power_converged"]):
+            if p and not c:
+                warnings.warn(f"power method did not converge within {p} iterations",
+                              RuntimeWarning)
+    for neg in col["merit_negative"]:
+        if neg:
+            warnings.warn("negative quadratic form in the merit: lambda may underestimate "
+                          "lambda_1(AA*)", RuntimeWarning)
+    ro, co = pk.row_off.tolist(), pk.col_off.tolist()
+    nlog = [min(v, MAX_LOG) for v in col["n_log"]]
+    lmax = max(nlog) if nlog else 0
+    rec_cols = {f: recs[f][:, :lmax].tolist() for f in recs.dtype.names}
+    out = []
+    for i in range(pk.count):
+        k = kkts[i]
+        kkt = KktResidual(k[0], k[1], k[2], k[3], k[4], k[5], k[6], k[7], k[8],
+                          col["dual_clamped"][i])
+        log = [RestartEvent(rec_cols["outer_index"][i][q], _TRIGGER[rec_cols["trigger"][i][q]],
+                            rec_cols["tau"][i][q], rec_cols["sigma_next"][i][q],
+                            rec_cols["merit"][i][q]) for q in range(nlog[i])]
+        sol = PrimalDualPoint(y=y[ro[i]:ro[i + 1]], z=z[co[i]:co[i + 1]], x=x[co[i]:co[i + 1]])
+        out.append(SolveReport(
+            status=_STATUS[col["status"][i]], primal_objective=col["primal_objective"][i],
+            dual_objective=col["dual_objective"][i], kkt=kkt, iterations=col["iterations"][i],
+            restarts=col["restarts"][i], restart_log=log,
+            timings=Timings(iteration_seconds=col["device_seconds"][i]), solution=sol,
+            sigma_final=col["sigma_final"][i], lambda_estimate=col["lambda_estimate"][i],
+            device_stats={"lambda_raw": col["lambda_raw"][i],
+                          "power_iterations": col["power_iterations"][i],
+                          "b_factor": col["b_factor"][i], "c_factor": col["c_factor"][i],
+                          "batch_index": i}))
+    return out
 
 
 def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
