@@ -1376,14 +1376,15 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
       } else {
         rc = launch_sell(c, c->mat_at(true), v, et, P.powt, nullptr);
       }
-      if (!rc) rc = launch_sell(c, c->mat_a(true), u, ea, P.powa, &ga);
+      // A u with the power step in its last CTA, then v = w / ||w||
+      EpiPowAStep eas{};
+      static_cast<EpiPowA &>(eas) = ea;
+      if (!rc) rc = launch_sell(c, c->mat_a(true), u, eas, P.powa, &ga);
       if (rc) {
         cudaStreamEndCapture(s, &g);
         return rc;
       }
-      k_pow_step<<<1, kThreads, 0, s>>>(P.powa, ga, c->pow);
       k_pow_norm<<<grid_for(m), 256, 0, s>>>(wv, v, m, c->pow);
-      k_pow_norm_done<<<1, 1, 0, s>>>(c->pow);
     }
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("pow capture: ") + cudaGetErrorString(e));
@@ -1395,7 +1396,7 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
   }
   for (;;) {
     CK(cudaGraphLaunch(c->pow_graph, s));
-    c->launches += 5 * kPowBatch;
+    c->launches += 3 * kPowBatch;
     CK(cudaMemcpyAsync(c->h_pow, c->pow, sizeof(PowState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (c->h_pow->done) break;

@@ -149,7 +149,8 @@ struct IterParams {
 // Power-method state (sparse.py:184-198), advanced entirely on the device.
 struct PowState {
   double lam, lam_prev, nw, tol;
-  int iters, max_iters, converged, done, norm_pending, pad_;
+  int iters, max_iters, converged, done, norm_pending;
+  unsigned arrive;                  // CTAs of the fused A u + power-step launch (EpiPowA)
 };
 
 // ---------------------------------------------------------------------------
@@ -217,6 +218,15 @@ template <class E, class = void>
 struct has_init : std::false_type {};
 template <class E>
 struct has_init<E, std::void_t<decltype(std::declval<E &>().init(0))>> : std::true_type {};
+
+// An epilogue with final(part, nparts) runs it in the LAST CTA of the launch to
+// finish (ticket counter), after every CTA's partials are stored: the
+// fixed-order reduction and the scalar step fused into the product kernel.
+template <class E, class = void>
+struct has_final : std::false_type {};
+template <class E>
+struct has_final<E, std::void_t<decltype(std::declval<E &>().final(nullptr, 0))>>
+    : std::true_type {};
 
 template <int U, bool GA, class Epi>
 __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
@@ -412,6 +422,17 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += gridDim.x * kWarpsPerCta)
     long_row(M, M.long_rows[li], lane, xg, epi, acc, pol);
   if constexpr (Epi::NQ > 0) block_reduce_store<Epi::NQ>(acc, part, gridDim.x);
+  if constexpr (has_final<Epi>::value) {
+    __shared__ unsigned ticket;
+    __threadfence();                     // this CTA's partials before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) ticket = atomicAdd(epi.arrive_counter(), 1u);
+    __syncthreads();
+    if (ticket == gridDim.x - 1) {
+      __threadfence();                   // every CTA's partials visible
+      epi.final(part, gridDim.x);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -698,7 +719,7 @@ struct EpiPowA {
   static constexpr int NQ = 2;
   const double *v;
   double *wv;
-  const PowState *S;
+  PowState *S;
   double vi;
   __device__ bool enter() { return !S->done; }
   __device__ void prefetch(int i) { vi = v[i]; }
@@ -732,8 +753,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_final(RedList L, double *ou
 
 // one CTA: reduce the v.w and w.w partials in fixed order, then the scalar
 // logic of one power step (sparse.py:188-198).
-__global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int nparts, PowState *S) {
-  if (S->done) return;
+__device__ __forceinline__ void pow_step_block(const double *part, int nparts, PowState *S) {
   double a[2] = {0.0, 0.0};
   for (int i = threadIdx.x; i < nparts; i += kThreads) {
     a[0] = __dadd_rn(a[0], part[i]);
@@ -746,11 +766,13 @@ __global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int n
     S->iters += 1;
     S->lam = lam;
     S->nw = nw;
+    S->arrive = 0;
     if (nw == 0.0) {
       S->done = 1;                       // break before v = w / nw
+      S->norm_pending = 0;
       return;
     }
-    S->norm_pending = 1;                 // v = w / nw
+    S->norm_pending = 1;                 // v = w / nw (k_pow_norm; recomputing it is idempotent)
     if (S->iters > 1 && fabs(__dsub_rn(lam, S->lam_prev)) <=
                             __dmul_rn(S->tol, fmax(fabs(lam), 1e-300))) {
       S->converged = 1;
@@ -761,6 +783,17 @@ __global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int n
     }
   }
 }
+
+__global__ void __launch_bounds__(kThreads) k_pow_step(const double *part, int nparts, PowState *S) {
+  if (S->done) return;
+  pow_step_block(part, nparts, S);
+}
+
+// EpiPowA whose last CTA also runs the power step (k_pow_step fused in)
+struct EpiPowAStep : EpiPowA {
+  __device__ unsigned *arrive_counter() { return &S->arrive; }
+  __device__ void final(const double *part, int nparts) { pow_step_block(part, nparts, S); }
+};
 
 __global__ void k_pow_norm(const double *__restrict__ wv, double *__restrict__ v, int m,
                            PowState *S) {
