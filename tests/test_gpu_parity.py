@@ -133,6 +133,36 @@ def test_iteration_bit_exact_midsize(engine, monkeypatch):
     dev.close()
 
 
+@pytest.mark.parametrize("shape", ["c1", "long_rows"])
+def test_spmv_abi_bit_exact(shape):
+    """hpr_spmv (the exact path's A x / A^T y) is bit-identical to the oracle's
+    sequential csr_matvec on the current (unscaled) values."""
+    import torch
+    rng = np.random.default_rng(3)
+    if shape == "c1":
+        prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    else:
+        a = rng.uniform(-1, 1, (30, 3000))
+        a[rng.uniform(size=a.shape) < 0.5] = 0.0          # rows of ~1500 entries (long rows)
+        prob = P.LpProblem.from_dense(a[:10], np.ones(10), a[10:], np.zeros(20),
+                                      rng.uniform(-1, 1, 3000))
+    dev = _dev(prob, 0, False, False)
+    olp = O.OracleLP.from_problem(prob)
+    x = rng.normal(size=olp.n)
+    y = rng.normal(size=olp.m)
+    with torch.cuda.stream(dev.stream):
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.from_numpy(y).cuda()
+        ax = torch.empty(olp.m, dtype=torch.float64, device="cuda")
+        aty = torch.empty(olp.n, dtype=torch.float64, device="cuda")
+        dev.spmv(False, xd, ax)
+        dev.spmv(True, yd, aty)
+    dev.stream.synchronize()
+    assert np.array_equal(ax.cpu().numpy(), olp.a.matvec(x))
+    assert np.array_equal(aty.cpu().numpy(), olp.transpose().matvec(y))
+    dev.close()
+
+
 def test_scaling_and_power_vs_oracle():
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     dev = _dev(prob)
