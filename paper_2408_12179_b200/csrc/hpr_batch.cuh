@@ -236,22 +236,28 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   const int tz = (int)z0;
 
   // ---- position-major shared-memory copies of A and A^T ----
-  // ranks by (length desc, index asc)
+  // ranks by (length desc, index asc); the lengths are staged in shared
+  // memory first (yb / xb as scratch: written again before their first use),
+  // so the all-pairs rank loop reads broadcast shared-memory words
+  int *lenA = (int *)yb, *lenT = (int *)xb;
+  for (int i = tid; i < m; i += kBT) lenA[i] = grp[i + 1] - grp[i];
+  for (int j = tid; j < n; j += kBT) lenT[j] = gtrp[j + 1] - gtrp[j];
+  __syncthreads();
   for (int i = tid; i < m; i += kBT) {
-    const int li = grp[i + 1] - grp[i];
+    const int li = lenA[i];
     int rank = 0;
     for (int q = 0; q < m; ++q) {
-      const int lq = grp[q + 1] - grp[q];
+      const int lq = lenA[q];
       rank += (lq > li) || (lq == li && q < i);
     }
     aperm[rank] = (u16)i;
     alen[rank] = (u16)li;
   }
   for (int j = tid; j < n; j += kBT) {
-    const int lj = gtrp[j + 1] - gtrp[j];
+    const int lj = lenT[j];
     int rank = 0;
     for (int q = 0; q < n; ++q) {
-      const int lq = gtrp[q + 1] - gtrp[q];
+      const int lq = lenT[q];
       rank += (lq > lj) || (lq == lj && q < j);
     }
     atperm[rank] = (u16)j;
