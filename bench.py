@@ -110,6 +110,31 @@ def gather_roofline(nnz, iterations, seconds, lay=None):
             "frac": achieved / peak, "note": note}
 
 
+def smem_roofline(probs, lp_its_per_s):
+    """C5: the batch kernel works out of each SM's shared memory (the LP is
+    staged once per solve), so its bound is the shared-memory port, 128 B per
+    cycle per SM.  Algorithmic shared-memory bytes per LP-iteration: A and A^T
+    values + 16-bit columns (10 B per nonzero each) and one 8-byte operand
+    gather per nonzero in each phase, plus the x-phase's 7 and the y-phase's 4
+    n / m-vector accesses (x, anchor, c, l, u read, w, x written; y, anchor, b
+    read, y written)."""
+    import torch
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    mhz = float(json.load(open(p)).get("sm_max_mhz", 1965.0)) if os.path.exists(p) else 1965.0
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    m = sum(q.m for q in probs) / len(probs)
+    n = sum(q.n for q in probs) / len(probs)
+    nnz = sum(q.a_eq.nnz + q.a_ineq.nnz for q in probs) / len(probs)
+    per_it = 2 * nnz * (10 + 8) + 8 * (7 * n + 4 * m)
+    peak = sms * 128 * mhz * 1e6 / 1e9
+    achieved = per_it * lp_its_per_s / 1e9
+    return {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "k_batch_solve (whole solve per CTA, LP resident in shared memory)",
+            "bytes_per_lp_iteration": per_it,
+            "peak_source": "148 SMs x 128 B/cycle x max SM clock (architectural)"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -514,7 +539,7 @@ def run_c5(args, dist, ws, rank, local):
                        "step": "the rank's shard solved to 1e-8 in one launch (one LP per CTA)",
                        "status": st, "l2": "inputs re-read from HBM each step (490 MB > L2)",
                        "parallelism": f"batch sharded x{ws}" if ws > 1 else "single GPU"},
-            "roofline": None,
+            "roofline": smem_roofline(probs, value),
             "cpu_baseline": cpu,
             "e2e": {"value": its_e2e / t_e2e, "unit": "LP-it/s",
                     "h2d_bytes_per_step": pk.h2d_bytes(),

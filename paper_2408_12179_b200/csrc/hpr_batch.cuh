@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   // memory first (yb / xb as scratch: written again before their first use),
   // so the all-pairs rank loop reads broadcast shared-memory words
   int *lenA = (int *)yb, *lenT = (int *)xb;
+  u16 *rankA = (u16 *)ay, *rankT = (u16 *)ax;   // row / column -> position (scratch too)
   for (int i = tid; i < m; i += kBT) lenA[i] = grp[i + 1] - grp[i];
   for (int j = tid; j < n; j += kBT) lenT[j] = gtrp[j + 1] - gtrp[j];
   __syncthreads();
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     }
     aperm[rank] = (u16)i;
     alen[rank] = (u16)li;
+    rankA[i] = (u16)rank;
   }
   for (int j = tid; j < n; j += kBT) {
     const int lj = lenT[j];
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     }
     atperm[rank] = (u16)j;
     atlen[rank] = (u16)lj;
+    rankT[j] = (u16)rank;
   }
   __syncthreads();
   if (tid == 0) {                                // row starts, every row padded to odd length
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     const int i = aperm[q], g0 = grp[i], L = alen[q], o = ast[q];
     for (int k2 = 0; k2 < L; ++k2) {
       av[o + k2] = gval[g0 + k2];
-      aci[o + k2] = (u16)gci[g0 + k2];
+      aci[o + k2] = rankT[gci[g0 + k2]];     // column ids -> A^T positions
     }
     if (!(L & 1)) {
       av[o + L] = 0.0;
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     const int j = atperm[q], g0 = gtrp[j] - tz, L = atlen[q], o = atst[q];
     for (int k2 = 0; k2 < L; ++k2) {
       atv[o + k2] = gtval[g0 + k2];
-      atci[o + k2] = (u16)gtci[g0 + k2];
+      atci[o + k2] = rankA[gtci[g0 + k2]];   // row ids -> A positions
     }
     if (!(L & 1)) {
       atv[o + L] = 0.0;
@@ -307,18 +310,18 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   // ---- scale_problem (scaling.py:81-103) ----
   // one pass: row divisors in yb, column divisors in xb, then both value copies
   // become (v / dr[row]) / dc[col]
-  // (loops run over positions q: row aperm[q] / column atperm[q])
+  // (POSITION SPACE: every m-vector is indexed by the A position q of row
+  // aperm[q], every n-vector by the A^T position of column atperm[q]; the
+  // stored column ids are positions too, so all loops below are coalesced)
   auto apply_pass = [&]() {
     for (int q = tid; q < m; q += kBT) {
-      const int i = aperm[q];
-      const double d = yb[i];
-      rs[i] = __dmul_rn(rs[i], d);
+      const double d = yb[q];
+      rs[q] = __dmul_rn(rs[q], d);
       for (int e = ast[q]; e < ast[q] + alen[q]; ++e) av[e] = __ddiv_rn(__ddiv_rn(av[e], d), xb[aci[e]]);
     }
     for (int q = tid; q < n; q += kBT) {
-      const int j = atperm[q];
-      const double d = xb[j];
-      csc[j] = __dmul_rn(csc[j], d);
+      const double d = xb[q];
+      csc[q] = __dmul_rn(csc[q], d);
       for (int e = atst[q]; e < atst[q] + atlen[q]; ++e)
         atv[e] = __ddiv_rn(__ddiv_rn(atv[e], yb[atci[e]]), d);
     }
@@ -329,13 +332,13 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       double mx = 0.0;
       for (int e = ast[q]; e < ast[q] + alen[q]; ++e) mx = fmax(mx, fabs(av[e]));
       double d = sqrt(mx);
-      yb[aperm[q]] = d == 0.0 ? 1.0 : d;
+      yb[q] = d == 0.0 ? 1.0 : d;
     }
     for (int q = tid; q < n; q += kBT) {
       double mx = 0.0;
       for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) mx = fmax(mx, fabs(atv[e]));
       double d = sqrt(mx);
-      xb[atperm[q]] = d == 0.0 ? 1.0 : d;
+      xb[q] = d == 0.0 ? 1.0 : d;
     }
     __syncthreads();
     apply_pass();
@@ -345,22 +348,23 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       double s = 0.0;
       for (int e = ast[q]; e < ast[q] + alen[q]; ++e) s = __dadd_rn(s, fabs(av[e]));
       double d = sqrt(s);
-      yb[aperm[q]] = d == 0.0 ? 1.0 : d;
+      yb[q] = d == 0.0 ? 1.0 : d;
     }
     for (int q = tid; q < n; q += kBT) {
       double s = 0.0;
       for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) s = __dadd_rn(s, fabs(atv[e]));
       double d = sqrt(s);
-      xb[atperm[q]] = d == 0.0 ? 1.0 : d;
+      xb[q] = d == 0.0 ? 1.0 : d;
     }
     __syncthreads();
     apply_pass();
   }
-  for (int i = tid; i < m; i += kBT) bs[i] = __ddiv_rn(b0[i], rs[i]);
-  for (int j = tid; j < n; j += kBT) {
-    cs[j] = __ddiv_rn(c0v[j], csc[j]);
-    ls[j] = __dmul_rn(l0[j], csc[j]);
-    us[j] = __dmul_rn(u0[j], csc[j]);
+  for (int q = tid; q < m; q += kBT) bs[q] = __ddiv_rn(b0[aperm[q]], rs[q]);
+  for (int q = tid; q < n; q += kBT) {
+    const int j = atperm[q];
+    cs[q] = __ddiv_rn(c0v[j], csc[q]);
+    ls[q] = __dmul_rn(l0[j], csc[q]);
+    us[q] = __dmul_rn(u0[j], csc[q]);
   }
   __syncthreads();
   double bf = 1.0, cf = 1.0;
@@ -383,8 +387,8 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   double bnorm, cnorm;
   {
     double v2[2] = {0.0, 0.0};
-    for (int i = tid; i < m; i += kBT) v2[0] = __dadd_rn(v2[0], sq(C.term_original ? b0[i] : bs[i]));
-    for (int j = tid; j < n; j += kBT) v2[1] = __dadd_rn(v2[1], sq(C.term_original ? c0v[j] : cs[j]));
+    for (int q = tid; q < m; q += kBT) v2[0] = __dadd_rn(v2[0], sq(C.term_original ? b0[aperm[q]] : bs[q]));
+    for (int q = tid; q < n; q += kBT) v2[1] = __dadd_rn(v2[1], sq(C.term_original ? c0v[atperm[q]] : cs[q]));
     bsum<2>(v2, red);
     bnorm = sqrt(v2[0]);
     cnorm = sqrt(v2[1]);
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   // ---- power method (sparse.py:165-203): v in yb, u in w, A u in ay ----
   int start = -2;
   for (int fb = -1; fb < m; ++fb) {
-    for (int i = tid; i < m; i += kBT) yb[i] = fb < 0 ? 1.0 : (i == fb ? 1.0 : 0.0);
+    for (int q = tid; q < m; q += kBT) yb[q] = fb < 0 ? 1.0 : ((int)aperm[q] == fb ? 1.0 : 0.0);
     __syncthreads();
     double u2[1] = {0.0};
     for (int q = tid; q < n; q += kBT) u2[0] = __dadd_rn(u2[0], sq(srow(atst, atlen, atci, atv, yb, q)));
@@ -416,14 +420,13 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   if (start != -2) {
     for (int it = 1; it <= C.power_max; ++it) {
       piters = it;
-      for (int q = tid; q < n; q += kBT) w[atperm[q]] = srow(atst, atlen, atci, atv, yb, q);
+      for (int q = tid; q < n; q += kBT) w[q] = srow(atst, atlen, atci, atv, yb, q);
       __syncthreads();
       double d2[2] = {0.0, 0.0};
       for (int q = tid; q < m; q += kBT) {
-        const int i = aperm[q];
         const double s = srow(ast, alen, aci, av, w, q);
-        ay[i] = s;
-        d2[0] = __dadd_rn(d2[0], __dmul_rn(yb[i], s));
+        ay[q] = s;
+        d2[0] = __dadd_rn(d2[0], __dmul_rn(yb[q], s));
         d2[1] = __dadd_rn(d2[1], sq(s));
       }
       bsum<2>(d2, red);
@@ -462,8 +465,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
   auto kkt = [&](double (&s)[11]) {
     for (int q = tid; q < m; q += kBT) {
       const int i = aperm[q];
-      const double axi = term_orig ? grow(grp, 0, gci, gval, ox, i) : srow(ast, alen, aci, av, ox, q);
-      const double bi = term_orig ? b0[i] : bs[i];
+      // scaled termination space: the candidate is (yb, xb) in shared memory
+      const double axi = term_orig ? grow(grp, 0, gci, gval, ox, i) : srow(ast, alen, aci, av, xb, q);
+      const double bi = term_orig ? b0[i] : bs[q];
       const double yi = oy[i];
       double prim = __dsub_rn(bi, axi);
       double tproj = __dadd_rn(__dsub_rn(yi, axi), bi);
@@ -477,10 +481,10 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     }
     for (int q = tid; q < n; q += kBT) {
       const int j = atperm[q];
-      const double aty = term_orig ? grow(gtrp, tz, gtci, gtval, oy, j) : srow(atst, atlen, atci, atv, oy, q);
-      const double cj = term_orig ? c0v[j] : cs[j];
-      const double l = term_orig ? l0[j] : ls[j];
-      const double u = term_orig ? u0[j] : us[j];
+      const double aty = term_orig ? grow(gtrp, tz, gtci, gtval, oy, j) : srow(atst, atlen, atci, atv, yb, q);
+      const double cj = term_orig ? c0v[j] : cs[q];
+      const double l = term_orig ? l0[j] : ls[q];
+      const double u = term_orig ? u0[j] : us[q];
       const double zj = oz[j], xj = ox[j];
       s[3] = __dadd_rn(s[3], sq(__dsub_rn(__dsub_rn(cj, aty), zj)));
       s[4] = __dadd_rn(s[4], __dmul_rn(cj, xj));
@@ -546,16 +550,14 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       const double wn = wtab[2 * (st % kWTab)], wa = wtab[2 * (st % kWTab) + 1];
       int bad = 0;
       for (int q = tid; q < n; q += 2 * kBT) {   // x phase (core.py:168-169), 2 columns
-        const int j = atperm[q];
         const int q2 = q + kBT < n ? q + kBT : -1;
-        const int j2 = q2 >= 0 ? atperm[q2] : -1;
         double aty0, aty1;
         srow2(atst, atlen, atci, atv, y, q, q2, aty0, aty1);
         for (int h = 0; h < 2; ++h) {
-        const int jj = h ? j2 : j;
+        const int jj = h ? q2 : q;
         if (jj < 0) break;
         const double aty = h ? aty1 : aty0;
-        const int j = jj;
+        const int j = jj;                        // position
         const double xj = x[j];
         const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
         const double xbj = np_clip(v, ls[j], us[j]);
@@ -569,17 +571,16 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
       }
       __syncthreads();
       for (int q = tid; q < m; q += kBT) {       // y phase (core.py:170-172)
-        const int i = aperm[q];
         const double s = srow(ast, alen, aci, av, w, q);
-        const double yi = y[i];
-        double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
-        if (i >= m1) ybi = np_max(ybi, 0.0);
+        const double yi = y[q];
+        double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[q], s), lamsig));
+        if (aperm[q] >= m1) ybi = np_max(ybi, 0.0);
         double yn = ybi;
         if (C.variant != 0) {
           const double tg = C.variant == 2 ? __dsub_rn(__dmul_rn(2.0, ybi), yi) : ybi;
-          yn = __dadd_rn(__dmul_rn(wa, ay[i]), __dmul_rn(wn, tg));
+          yn = __dadd_rn(__dmul_rn(wa, ay[q]), __dmul_rn(wn, tg));
         }
-        y[i] = yn;
+        y[q] = yn;
         bad |= !isfinite(yn);
       }
       if (__syncthreads_or(bad)) {              // NumericalBreakdownError(k)
@@ -602,18 +603,18 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
 #pragma unroll
     for (int q = 0; q < 17; ++q) s17[q] = 0.0;
     for (int q = tid; q < n; q += kBT) {
-      const int j = atperm[q];
+      const int j = atperm[q];                   // column (global arrays), q: position
       const double aty = srow(atst, atlen, atci, atv, y, q);
-      const double xj = x[j];
-      const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[j])));
-      const double xbj = np_clip(v, ls[j], us[j]);
+      const double xj = x[q];
+      const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cs[q])));
+      const double xbj = np_clip(v, ls[q], us[q]);
       const double zbj = __ddiv_rn(__dsub_rn(xbj, v), sigma);
-      xb[j] = xbj;
-      w[j] = __dsub_rn(__dmul_rn(2.0, xbj), xj);
-      s17[0] = __dadd_rn(s17[0], sq(__dsub_rn(xbj, ax[j])));     // bar_dx2
+      xb[q] = xbj;
+      w[q] = __dsub_rn(__dmul_rn(2.0, xbj), xj);
+      s17[0] = __dadd_rn(s17[0], sq(__dsub_rn(xbj, ax[q])));     // bar_dx2
       s17[1] = __dadd_rn(s17[1], sq(__dsub_rn(xj, xbj)));        // dx2
       if (term_orig) {
-        const double cj = csc[j];
+        const double cj = csc[q];
         ox[j] = np_clip(__dmul_rn(xbj, __ddiv_rn(bf, cj)), l0[j], u0[j]);
         oz[j] = __dmul_rn(zbj, __dmul_rn(cf, cj));
       } else {
@@ -623,25 +624,24 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     }
     __syncthreads();
     for (int q = tid; q < m; q += kBT) {
-      const int i = aperm[q];
+      const int i = aperm[q];                    // row (global arrays), q: position
       const double s = srow(ast, alen, aci, av, w, q);
-      const double yi = y[i];
-      double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[i], s), lamsig));
+      const double yi = y[q];
+      double ybi = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bs[q], s), lamsig));
       if (i >= m1) ybi = np_max(ybi, 0.0);
       const double dyi = __dsub_rn(yi, ybi);
-      yb[i] = ybi;
-      gdy[i] = dyi;
+      yb[q] = ybi;
+      gdy[q] = dyi;                              // by position (gathered through atci)
       s17[2] = __dadd_rn(s17[2], sq(dyi));                       // dy2
-      s17[3] = __dadd_rn(s17[3], sq(__dsub_rn(ybi, ay[i])));     // bar_dy2
-      oy[i] = term_orig ? __dmul_rn(ybi, __ddiv_rn(cf, rs[i])) : ybi;
+      s17[3] = __dadd_rn(s17[3], sq(__dsub_rn(ybi, ay[q])));     // bar_dy2
+      oy[i] = term_orig ? __dmul_rn(ybi, __ddiv_rn(cf, rs[q])) : ybi;
     }
     __syncthreads();
     // merit terms (core.py:191-197): A^T dy
     for (int q = tid; q < n; q += kBT) {
-      const int j = atperm[q];
       double a = 0.0;
       for (int e = atst[q]; e < atst[q] + atlen[q]; ++e) a = __dadd_rn(a, __dmul_rn(atv[e], gdy[atci[e]]));
-      const double dx = __dsub_rn(x[j], xb[j]);
+      const double dx = __dsub_rn(x[q], xb[q]);
       s17[4] = __dadd_rn(s17[4], sq(__dadd_rn(dx, __dmul_rn(sigma, a))));   // sh2
       s17[5] = __dadd_rn(s17[5], sq(a));                                    // aty2
     }
@@ -718,10 +718,15 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
 
   // ---- finish (driver.py:374-391) ----
   if (!have_ckpt) {     // breakdown before the first checkpoint: the origin
-    for (int i = tid; i < m; i += kBT) oy[i] = 0.0;
-    for (int j = tid; j < n; j += kBT) {
+    for (int q = tid; q < m; q += kBT) {
+      oy[aperm[q]] = 0.0;
+      yb[q] = 0.0;                               // the scaled candidate kkt() reads
+    }
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
       oz[j] = 0.0;
-      ox[j] = np_clip(0.0, term_orig ? l0[j] : ls[j], term_orig ? u0[j] : us[j]);
+      ox[j] = np_clip(0.0, term_orig ? l0[j] : ls[q], term_orig ? u0[j] : us[q]);
+      xb[q] = ox[j];
     }
     __syncthreads();
     double s11[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -730,9 +735,13 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     kkt_finish(s11);
   }
   if (!term_orig) {     // unscale + clip (driver.py:382-386)
-    for (int i = tid; i < m; i += kBT) oy[i] = __dmul_rn(oy[i], __ddiv_rn(cf, rs[i]));
-    for (int j = tid; j < n; j += kBT) {
-      const double cj = csc[j];
+    for (int q = tid; q < m; q += kBT) {
+      const int i = aperm[q];
+      oy[i] = __dmul_rn(oy[i], __ddiv_rn(cf, rs[q]));
+    }
+    for (int q = tid; q < n; q += kBT) {
+      const int j = atperm[q];
+      const double cj = csc[q];
       ox[j] = np_clip(__dmul_rn(ox[j], __ddiv_rn(bf, cj)), l0[j], u0[j]);
       oz[j] = __dmul_rn(oz[j], __dmul_rn(cf, cj));
     }
