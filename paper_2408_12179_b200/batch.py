@@ -12,6 +12,7 @@ checkpoints, restarts and sigma updates without returning to the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import warnings
 
@@ -64,8 +65,48 @@ class PackedBatch:
         self.row_off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int64)
         self.col_off = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
         self.nz_off = np.concatenate([[0], np.cumsum(nzs)]).astype(np.int64)
+        if os.environ.get("HPR_PACK_LOOP") == "1":
+            rp, ci, val, b, c, lo, up = self._pack_loop(problems, ns, nzs)
+        else:
+            rp, ci, val, b, c, lo, up = self._pack_concat(problems)
+        self.arrays = {
+            "row_off": self.row_off, "col_off": self.col_off, "nz_off": self.nz_off,
+            "m1": m1s, "rp": rp, "ci": ci, "val": val, "b": b, "c": c, "lower": lo, "upper": up,
+            "obj_const": oc, "obj_neg": neg}
+
+    def _pack_concat(self, problems):
+        """Each batch array is one np.concatenate over the LPs' pieces (the
+        copies and the int64 -> int32 casts run in C)."""
+        tops = [p.a_eq for p in problems]
+        bots = [p.a_ineq for p in problems]
+        pieces, shift, lens = [], [], []
+        for t, b in zip(tops, bots):
+            tr, br = np.asarray(t.row_offsets), np.asarray(b.row_offsets)
+            nt = int(tr[-1] - tr[0])
+            pieces.append(tr)
+            pieces.append(br[1:])
+            shift.append(-int(tr[0]))
+            shift.append(nt - int(br[0]))
+            lens.append(len(tr))
+            lens.append(len(br) - 1)
+        rp = np.concatenate(pieces, dtype=np.int32, casting="unsafe")
+        rp += np.repeat(np.asarray(shift, np.int32), lens)
+        ci = np.concatenate([x for t, b in zip(tops, bots)
+                             for x in (t.col_indices, b.col_indices)], dtype=np.int32,
+                            casting="unsafe")
+        val = np.concatenate([x for t, b in zip(tops, bots) for x in (t.values, b.values)],
+                             dtype=np.float64)
+        b = np.concatenate([x for p in problems for x in (p.b_eq, p.b_ineq)], dtype=np.float64)
+        c = np.concatenate([p.c for p in problems], dtype=np.float64)
+        lo = np.concatenate([p.lower for p in problems], dtype=np.float64)
+        up = np.concatenate([p.upper for p in problems], dtype=np.float64)
+        return rp, ci, val, b, c, lo, up
+
+    def _pack_loop(self, problems, ns, nzs):
+        """Per-LP slice assignments into preallocated arrays (HPR_PACK_LOOP=1)."""
+        cnt = self.count
         R, C, Z = int(self.row_off[-1]), int(self.col_off[-1]), int(self.nz_off[-1])
-        rp = np.empty(R + cnt, np.int64)           # cast to int32 once, vectorised
+        rp = np.empty(R + cnt, np.int64)
         ci = np.empty(Z, np.int64)
         val = np.empty(Z, np.float64)
         b = np.empty(R, np.float64)
@@ -90,10 +131,7 @@ class PackedBatch:
             c[c0:c0 + n] = p.c
             lo[c0:c0 + n] = p.lower
             up[c0:c0 + n] = p.upper
-        self.arrays = {
-            "row_off": self.row_off, "col_off": self.col_off, "nz_off": self.nz_off,
-            "m1": m1s, "rp": rp.astype(np.int32), "ci": ci.astype(np.int32), "val": val, "b": b, "c": c, "lower": lo, "upper": up,
-            "obj_const": oc, "obj_neg": neg}
+        return rp.astype(np.int32), ci.astype(np.int32), val, b, c, lo, up
 
     def h2d_bytes(self):
         return sum(a.nbytes for a in self.arrays.values())
