@@ -55,6 +55,9 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_L2KEEP
 #define HPR_L2KEEP 4    // matrix L2 policy: 0 evict_first, 1 keep A, 2 keep A^T, 3 normal, 4 auto
 #endif
+#ifndef HPR_SELL_U
+#define HPR_SELL_U 4    // entries per lane per batch without gather-ahead (2 / 8: C3 +20 % / +100 %)
+#endif
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
@@ -450,7 +453,7 @@ template <class Epi>
 int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
                 int *grid_out, bool pdl = false) {
   return M.ga ? launch_sell_u<4, true>(c, M, xg, epi, part, grid_out, pdl)
-              : launch_sell_u<4, false>(c, M, xg, epi, part, grid_out, pdl);
+              : launch_sell_u<HPR_SELL_U, false>(c, M, xg, epi, part, grid_out, pdl);
 }
 
 // The y-phase product A w with the phase epilogue: one SELL launch, or NB
