@@ -1200,8 +1200,8 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
   c->launches += 2;
   const int wg = grid_for((int64_t)m * 32);
   for (int it = 0; it < ruiz_iters; ++it) {  // sparse.py:216-223
-    k_row_maxabs<<<grid_for((int64_t)m * 32), 256, 0, s>>>(B.a_rp, B.a_val_s, m, dr);
-    k_col_maxabs<<<grid_for((int64_t)n * 32), 256, 0, s>>>(B.at_rp, B.at_perm, B.a_val_s, n, dc);
+    k_row_maxabs<<<grid_for(m), 256, 0, s>>>(B.a_rp, B.a_val_s, m, dr);
+    k_col_maxabs<<<grid_for(n), 256, 0, s>>>(B.at_rp, B.at_perm, B.a_val_s, n, dc);
     k_sqrt_div<<<grid_for(m), 256, 0, s>>>(dr, B.row_scale, m);
     k_sqrt_div<<<grid_for(n), 256, 0, s>>>(dc, B.col_scale, n);
     k_scale_vals<<<wg, 256, 0, s>>>(B.a_rp, B.a_ci, B.a_val_s, dr, dc, m);

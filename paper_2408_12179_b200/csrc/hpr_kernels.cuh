@@ -973,29 +973,19 @@ __global__ void k_sell_scatter(const int *sell_pos, const double *src, double *d
 }
 
 // Ruiz: per-row max |a| (exact; any order), per-column via the transpose perm.
-// (warp per row: coalesced reads, then a shuffle max -- fmax is exact and,
-// NaN-ignoring, order-independent, so the result equals the sequential one)
 __global__ void k_row_maxabs(const int *rp, const double *val, int nrows, double *out) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nrows; i += nw) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
     double mx = 0.0;
-    for (int k = rp[i] + lane; k < rp[i + 1]; k += 32) mx = fmax(mx, fabs(val[k]));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (lane == 0) out[i] = mx;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) mx = fmax(mx, fabs(val[k]));
+    out[i] = mx;
   }
 }
 __global__ void k_col_maxabs(const int *rpt, const int *perm, const double *val, int ncols,
                              double *out) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < ncols; j += nw) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += gridDim.x * blockDim.x) {
     double mx = 0.0;
-    for (int k = rpt[j] + lane; k < rpt[j + 1]; k += 32) mx = fmax(mx, fabs(val[perm[k]]));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (lane == 0) out[j] = mx;
+    for (int k = rpt[j]; k < rpt[j + 1]; ++k) mx = fmax(mx, fabs(val[perm[k]]));
+    out[j] = mx;
   }
 }
 // Pock-Chambolle alpha = 1: sequential abs sums (np.add.at order, sparse.py:235,237).

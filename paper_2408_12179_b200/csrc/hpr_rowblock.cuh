@@ -650,8 +650,8 @@ int hpr_group_scale(hpr_group *g, int ruiz_iters, int pock_chambolle, int bc_nor
       const hpr_buffers &B = c->B;
       const int m = (int)c->d.m;
       if (ruiz) {
-        k_row_maxabs<<<grid_for((int64_t)m * 32), 256, 0, c->stream>>>(B.a_rp, B.a_val_s, m, c->dvec_m);
-        k_col_maxabs<<<grid_for((int64_t)n * 32), 256, 0, c->stream>>>(B.at_rp, B.at_perm, B.a_val_s, n, c->dvec_n);
+        k_row_maxabs<<<grid_for(m), 256, 0, c->stream>>>(B.a_rp, B.a_val_s, m, c->dvec_m);
+        k_col_maxabs<<<grid_for(n), 256, 0, c->stream>>>(B.at_rp, B.at_perm, B.a_val_s, n, c->dvec_n);
       } else {
         k_row_abssum<<<grid_for(m), 256, 0, c->stream>>>(B.a_rp, B.a_val_s, m, c->dvec_m);
         k_col_abssum<<<grid_for(n), 256, 0, c->stream>>>(B.at_rp, B.at_perm, B.a_val_s, n, c->dvec_n);
