@@ -634,7 +634,8 @@ def run_c4(args, dist, ws, rank, local):
                        "l2": "working set > L2 (no flush needed)",
                        "parallelism": f"row-block x{ws} (NCCL)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": load_traffic("c4") if args.c4_rows == 1_250_000 else None,
                          "kernel": "per-rank iteration (A_g^T partial + slice x-phase + A_g y-phase + collectives)",
                          "bytes_per_iteration": bi_rank, "peak_source": peak_kind},
             "cpu_baseline": None,
