@@ -163,6 +163,41 @@ def test_spmv_abi_bit_exact(shape):
     dev.close()
 
 
+def test_column_split_falls_back_for_very_long_block_rows(monkeypatch):
+    """A row with more than 65535 entries inside one column block cannot ride
+    the split layout's 16-bit slice lengths: the split is disabled and the
+    unsplit SELL path (long rows summed warp-cooperatively) gives the oracle's
+    bits."""
+    monkeypatch.setenv("HPR_CB", "0")
+    monkeypatch.setenv("HPR_STG", "0")
+    monkeypatch.setenv("HPR_SPLIT_COLS", "70000")
+    n = 140_000
+    rng = np.random.default_rng(5)
+    rows, cols, vals = [], [], []
+    rows += [0] * 70_000                          # 70000 entries in block 0
+    cols += list(range(0, 70_000))
+    vals += rng.uniform(0.5, 1.5, 70_000).tolist()
+    for i in range(1, 8):
+        cc = np.sort(rng.choice(n, size=50, replace=False))
+        rows += [i] * 50
+        cols += cc.tolist()
+        vals += rng.uniform(-1, 1, 50).tolist()
+    a = P.SparseMatrix.from_coo(rows, cols, vals, (8, n))
+    prob = P.LpProblem(a, P.SparseMatrix.from_coo([], [], [], (0, n)), np.ones(8), np.zeros(0),
+                       rng.uniform(0, 1, n), np.zeros(n), np.full(n, 2.0))
+    dev = _dev(prob)
+    assert dev.layout_info()["split_a"] == 0
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 1.0, lam)
+    dev.state_reset()
+    dev.run_inner(5, 0, 0, 1.0, lam, 2)
+    for _ in range(5):
+        O.iterate_once(st, slp)
+    assert np.array_equal(dev.to_host("y"), st.y) and np.array_equal(dev.to_host("x"), st.x)
+    dev.close()
+
+
 def test_scaling_and_power_vs_oracle():
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     dev = _dev(prob)
