@@ -61,7 +61,10 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
-constexpr int kPowBatch = 8;      // power steps per graph replay
+#ifndef HPR_POW_BATCH
+#define HPR_POW_BATCH 16   // 8 / 16 / 32 measured 17.55-17.73 / 17.78-17.79 / 17.76-17.78 k it/s on C2
+#endif
+constexpr int kPowBatch = HPR_POW_BATCH;   // power steps per graph replay
 constexpr int kMaxGridPerSm = 8;  // CTAs per SM cap of the SELL kernels (partials sizing)
 constexpr int kSumsqBlocks = 1024;
 
