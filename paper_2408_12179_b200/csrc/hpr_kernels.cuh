@@ -68,6 +68,24 @@ __device__ __forceinline__ int ld_stream(const int *ptr, uint64_t pol) {
   return v;
 }
 
+// Operand-vector gathers of the SELL kernels.  HPR_GATHER_LD selects the
+// load: 0 = ld.global.nc (L1-allocating), 1 = ld.global.nc without L1
+// allocation, 2 = ld.global.cg (L2 only).
+#ifndef HPR_GATHER_LD
+#define HPR_GATHER_LD 0
+#endif
+__device__ __forceinline__ double ld_gather(const double *ptr) {
+#if HPR_GATHER_LD == 1
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+#elif HPR_GATHER_LD == 2
+  return __ldcg(ptr);
+#else
+  return __ldg(ptr);
+#endif
+}
+
 // Row operands of the iteration epilogues (read once per iteration): with
 // HPR_EPI_NA they bypass L1 allocation so the gathered vector keeps the L1.
 #ifndef HPR_EPI_NA
@@ -258,7 +276,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
   double x0[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (u < len) x0[u] = __ldg(xg + c[u]);
+    if (u < len) x0[u] = ld_gather(xg + c[u]);
   int c1[U];
   double v1[U];
 #pragma unroll
@@ -271,7 +289,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
     double x1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (k + U + u < len) x1[u] = __ldg(xg + c1[u]);
+      if (k + U + u < len) x1[u] = ld_gather(xg + c1[u]);
     int c2[U];
     double v2[U];
 #pragma unroll
@@ -303,7 +321,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (k + u < len) xv[u] = __ldg(xg + c[u]);
+      if (k + u < len) xv[u] = ld_gather(xg + c[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
