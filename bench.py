@@ -299,16 +299,11 @@ def run_reference(args):
         return
     if args.config == "c4":
         from paper_2408_12179_b200.generators import generate_planted_block
-        from paper_2408_12179_b200 import LpProblem, SparseMatrix
         rows = args.c4_rows
         m1 = rows // 2
         rp, ci, va, b, ys, m1l, (lo, up, xs, zs), cpart = generate_planted_block(
             4, m1, rows - m1, C4_N, C4_PER_ROW, 0, rows)
-        c = cpart + zs
-        prob = LpProblem(a_eq=SparseMatrix.from_csr_arrays(rp[:m1 + 1], ci[:rp[m1]], va[:rp[m1]], m1, C4_N),
-                         a_ineq=SparseMatrix.from_csr_arrays(rp[m1:] - rp[m1], ci[rp[m1]:], va[rp[m1]:],
-                                                             rows - m1, C4_N),
-                         b_eq=b[:m1], b_ineq=b[m1:], c=c, lower=lo, upper=up)
+        prob = c4_lp((rp, ci, va, m1l, b, cpart + zs, lo, up), rows, m1)
         interval = 2
         tol = 1e-8
         power_max = 3          # per-iteration time does not depend on lambda's accuracy
@@ -569,6 +564,29 @@ def c4_block(rank, ws, rows_per_rank, local, dist):
     return (rp, ci, va, m1l, b, c, lo, up), m, m1, r0
 
 
+def c4_lp(block, m, m1):
+    """The one-rank C4 block (rows [0, m), the first m1 equalities) as an LpProblem."""
+    from paper_2408_12179_b200 import LpProblem, SparseMatrix
+    rp, ci, va, _m1l, b, c, lo, up = block
+    return LpProblem(a_eq=SparseMatrix.from_csr_arrays(rp[:m1 + 1], ci[:rp[m1]], va[:rp[m1]], m1, C4_N),
+                     a_ineq=SparseMatrix.from_csr_arrays(rp[m1:] - rp[m1], ci[rp[m1]:], va[rp[m1]:],
+                                                         m - m1, C4_N),
+                     b_eq=b[:m1], b_ineq=b[m1:], c=c, lower=lo, upper=up)
+
+
+def c4_cpu_sample(block, m, m1, iters=6):
+    """The oracle's C kernels (all host threads) on the one-rank C4 block:
+    setup (scaling, 3 power steps) untimed, then ``iters`` HPR iterations."""
+    O, scaled, st, threads = _oracle_setup(c4_lp(block, m, m1), 3)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        O.iterate_once(st, scaled)
+    dt = time.perf_counter() - t0
+    return {"value": iters / dt, "unit": "it/s", "cores": threads, "kind": "port",
+            "sample": f"{iters} HPR iterations of the same rank block (oracle C kernels, "
+                      f"OpenMP {threads} threads), setup excluded"}
+
+
 def run_c4(args, dist, ws, rank, local):
     import torch
     import paper_2408_12179_b200 as P
@@ -617,6 +635,35 @@ def run_c4(args, dist, ws, rank, local):
     its = interval * args.steps
     value = its / t_max               # every rank advances the same iterations
     nnz_rank = rows * C4_PER_ROW
+    grp.close()
+
+    # e2e through the public API from this rank's host block: every step
+    # uploads the block (pinned staging -> H2D), builds the rank group and runs
+    # solve() for two 150-iteration intervals (analyse, scale, power method,
+    # checkpoints, finalize, solution D2H); graphs are captured anew each time
+    import types
+    shell = types.SimpleNamespace(objective_constant=0.0, objective_negated=False)
+    cfg = P.SolverConfig(tolerance=1e-8, max_iterations=2 * interval, check_interval=interval)
+    e2e_t, e2e_its, h2d = 0.0, 0, 0
+    for _ in range(max(1, min(args.steps, 2))):
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nid = broadcast_nccl_id(rank) if dist is not None else nccl_unique_id()
+        g2 = RowBlockGroup.distributed(block, n=C4_N, m_total=m, m1_total=m1,
+                                       nnz_total=m * C4_PER_ROW, row0=r0, rank=rank, world=ws,
+                                       nccl_id=nid, device=local)
+        try:
+            rep = P.solve(shell, cfg, dev=g2)
+            torch.cuda.synchronize()
+            e2e_t += time.perf_counter() - t0
+            e2e_its += rep.iterations
+            h2d = g2.h2d_bytes
+        finally:
+            g2.close()
+    t_e2e, _ = _max_sum(dist, local, e2e_t, 0)
+    e2e_val = e2e_its / t_e2e
     peak, peak_kind = load_peaks()
     bi_rank = b_iter(rows, C4_N, nnz_rank)
     achieved = bi_rank * its / inner_s / 1e9
@@ -638,12 +685,13 @@ def run_c4(args, dist, ws, rank, local):
                          "traffic": load_traffic("c4") if args.c4_rows == 1_250_000 else None,
                          "kernel": "per-rank iteration (A_g^T partial + slice x-phase + A_g y-phase + collectives)",
                          "bytes_per_iteration": bi_rank, "peak_source": peak_kind},
-            "cpu_baseline": None,
-            "e2e": None,
+            "cpu_baseline": c4_cpu_sample(block, m, m1) if ws == 1 and not args.no_cpu else None,
+            "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 8 * (2 * C4_N + rows),
+                    "step": "upload + solve() for 300 iterations (setup included)"},
             "gpu_launches": launches,
             "clocks": sample_clocks.summary(),
         }
-    grp.close()
     _finish(dist, line, rank)
     return line
 
