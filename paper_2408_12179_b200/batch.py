@@ -39,7 +39,18 @@ class PackedBatch:
     """Host-side concatenation of a list of reference-shaped LPs (sizes first,
     then every LP's arrays copied into preallocated batch arrays)."""
 
-    def __init__(self, problems):
+    # upload order of the batch arrays (BatchRun lays them out in this order,
+    # each padded to 256 bytes)
+    ORDER = (("row_off", np.int64), ("col_off", np.int64), ("nz_off", np.int64),
+             ("m1", np.int32), ("rp", np.int32), ("ci", np.int32), ("val", np.float64),
+             ("b", np.float64), ("c", np.float64), ("lower", np.float64), ("upper", np.float64),
+             ("obj_const", np.float64), ("obj_neg", np.int32))
+
+    def __init__(self, problems, staging=None):
+        """``staging``: ``f(nbytes) -> uint8 numpy array`` (at least nbytes) to
+        pack into at the upload layout -- a pinned buffer: packing then writes
+        the bytes BatchRun copies to the device, with no second host copy and
+        no page faults on fresh arrays."""
         if not problems:
             raise ValueError("empty batch")
         cnt = len(problems)
@@ -65,18 +76,40 @@ class PackedBatch:
         self.row_off = np.concatenate([[0], np.cumsum(ms)]).astype(np.int64)
         self.col_off = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
         self.nz_off = np.concatenate([[0], np.cumsum(nzs)]).astype(np.int64)
+        R, C, Z = int(self.row_off[-1]), int(self.col_off[-1]), int(self.nz_off[-1])
+        lens = {"row_off": cnt + 1, "col_off": cnt + 1, "nz_off": cnt + 1, "m1": cnt,
+                "rp": R + cnt, "ci": Z, "val": Z, "b": R, "c": C, "lower": C, "upper": C,
+                "obj_const": cnt, "obj_neg": cnt}
+        out = {}
+        if staging is not None:
+            nbs = [lens[k] * np.dtype(dt).itemsize for k, dt in self.ORDER]
+            buf = staging(sum((nb + 255) // 256 * 256 for nb in nbs))
+            o = 0
+            for (k, dt), nb in zip(self.ORDER, nbs):
+                out[k] = buf[o:o + nb].view(dt)
+                o += (nb + 255) // 256 * 256
         if os.environ.get("HPR_PACK_LOOP") == "1":
             rp, ci, val, b, c, lo, up = self._pack_loop(problems, ns, nzs)
         else:
-            rp, ci, val, b, c, lo, up = self._pack_concat(problems)
+            rp, ci, val, b, c, lo, up = self._pack_concat(problems, out)
         self.arrays = {
             "row_off": self.row_off, "col_off": self.col_off, "nz_off": self.nz_off,
             "m1": m1s, "rp": rp, "ci": ci, "val": val, "b": b, "c": c, "lower": lo, "upper": up,
             "obj_const": oc, "obj_neg": neg}
+        for k, a in out.items():                 # the small arrays into the staging too
+            if self.arrays[k] is not a:
+                np.copyto(a, self.arrays[k], casting="unsafe")
+                self.arrays[k] = a
 
-    def _pack_concat(self, problems):
+    def _pack_concat(self, problems, out):
         """Each batch array is one np.concatenate over the LPs' pieces (the
-        copies and the int64 -> int32 casts run in C)."""
+        copies and the int64 -> int32 casts run in C), into ``out[name]`` when
+        given."""
+        def cat(name, parts, dt):
+            if name in out:
+                return np.concatenate(parts, out=out[name], casting="unsafe")
+            return np.concatenate(parts, dtype=dt, casting="unsafe")
+
         tops = [p.a_eq for p in problems]
         bots = [p.a_ineq for p in problems]
         pieces, shift, lens = [], [], []
@@ -89,17 +122,16 @@ class PackedBatch:
             shift.append(nt - int(br[0]))
             lens.append(len(tr))
             lens.append(len(br) - 1)
-        rp = np.concatenate(pieces, dtype=np.int32, casting="unsafe")
+        rp = cat("rp", pieces, np.int32)
         rp += np.repeat(np.asarray(shift, np.int32), lens)
-        ci = np.concatenate([x for t, b in zip(tops, bots)
-                             for x in (t.col_indices, b.col_indices)], dtype=np.int32,
-                            casting="unsafe")
-        val = np.concatenate([x for t, b in zip(tops, bots) for x in (t.values, b.values)],
-                             dtype=np.float64)
-        b = np.concatenate([x for p in problems for x in (p.b_eq, p.b_ineq)], dtype=np.float64)
-        c = np.concatenate([p.c for p in problems], dtype=np.float64)
-        lo = np.concatenate([p.lower for p in problems], dtype=np.float64)
-        up = np.concatenate([p.upper for p in problems], dtype=np.float64)
+        ci = cat("ci", [x for t, b in zip(tops, bots) for x in (t.col_indices, b.col_indices)],
+                 np.int32)
+        val = cat("val", [x for t, b in zip(tops, bots) for x in (t.values, b.values)],
+                  np.float64)
+        b = cat("b", [x for p in problems for x in (p.b_eq, p.b_ineq)], np.float64)
+        c = cat("c", [p.c for p in problems], np.float64)
+        lo = cat("lower", [p.lower for p in problems], np.float64)
+        up = cat("upper", [p.upper for p in problems], np.float64)
         return rp, ci, val, b, c, lo, up
 
     def _pack_loop(self, problems, ns, nzs):
@@ -180,7 +212,10 @@ class BatchRun:
         with _Staging.lock:
             stage = _Staging.get(total)
             host = stage.numpy()
+            base = host.ctypes.data
             for k, a in packed.arrays.items():
+                if a.ctypes.data == base + offs[k]:
+                    continue                      # packed in place (solve_batch)
                 host[offs[k]:offs[k] + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
             with torch.cuda.stream(self.stream):
                 self._inputs = torch.empty(total, dtype=torch.uint8, device=self.device)
@@ -283,7 +318,15 @@ def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
     if math.isfinite(cfg.time_limit_seconds):
         warnings.warn("batch time limits are measured per CTA on the device clock",
                       RuntimeWarning)
-    run = BatchRun(PackedBatch(list(problems)), device=device)
+    from .device import _Staging
+    if not _torch().cuda.is_available():
+        raise N.NativeUnavailableError("CUDA device required: the batch path has no CPU fallback")
+    problems = list(problems)
+    with _Staging.lock:
+        # pack straight into the pinned staging buffer, then one H2D copy
+        packed = PackedBatch(problems, staging=lambda nb: _Staging.get(nb).numpy())
+        run = BatchRun(packed, device=device)
+        packed.arrays = {}                        # views of the staging buffer: released
     run.launch(cfg)
     return run.reports(cfg)
 

@@ -38,7 +38,7 @@ class _Staging:
     reused across problems: no per-upload page-locking)."""
 
     buf = None
-    lock = threading.Lock()
+    lock = threading.RLock()
 
     @classmethod
     def get(cls, nbytes):

@@ -15,3 +15,8 @@ for rep in range(3):
     reps = run.reports(cfg); t4 = time.perf_counter()
     print(f"pack {1e3*(t1-t0):.1f} ms, upload+alloc {1e3*(t2-t1):.1f} ms, solve {1e3*(t3-t2):.1f} ms, "
           f"reports {1e3*(t4-t3):.1f} ms, total {1e3*(t4-t0):.1f} ms", flush=True)
+from paper_2408_12179_b200.batch import solve_batch
+for rep in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    reps = solve_batch(probs, cfg)
+    print(f"solve_batch (pack into pinned staging + upload + solve + reports) {1e3*(time.perf_counter()-t0):.1f} ms", flush=True)

@@ -52,6 +52,8 @@ def test_solve_fails_loudly_without_cuda():
     p = P.LpProblem.from_dense([[1.0]], [1.0], None, None, [1.0])
     with pytest.raises(NativeUnavailableError):
         P.solve(p)
+    with pytest.raises(NativeUnavailableError):
+        P.solve_batch([p, p])
 
 
 def test_product_does_not_import_oracle():
