@@ -188,6 +188,16 @@ def _config(cfg: SolverConfig, max_log: int) -> N.HprBatchConfig:
     return c
 
 
+_STREAMS = {}
+
+
+def _batch_stream(torch, device):
+    st = _STREAMS.get(device)
+    if st is None:
+        st = _STREAMS[device] = torch.cuda.Stream(device=torch.device("cuda", device))
+    return st
+
+
 class BatchRun:
     """Device residency of one packed batch + its native solve (re-runnable)."""
 
@@ -199,7 +209,9 @@ class BatchRun:
         self.packed = packed
         self.device = torch.device("cuda", device)
         self.dev_index = device
-        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        # one stream per device for every BatchRun: the caching allocator keeps
+        # freed blocks per stream, so a new stream per run would cudaMalloc anew
+        self.stream = stream if stream is not None else _batch_stream(torch, device)
         # one pinned staging buffer -> one H2D copy; the inputs are views of it
         from .device import _Staging
         tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
@@ -263,8 +275,16 @@ class BatchRun:
 
     def reports(self, cfg: SolverConfig) -> list[SolveReport]:
         self.stream.synchronize()
-        return _build_reports(self.packed, self.res.cpu().numpy(), self.log.cpu().numpy(),
-                              self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy())
+        # thousands of small report objects: no cyclic-GC passes while they are built
+        import gc
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            return _build_reports(self.packed, self.res.cpu().numpy(), self.log.cpu().numpy(),
+                                  self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy())
+        finally:
+            if was:
+                gc.enable()
 
 
 def _build_reports(pk: PackedBatch, raw, lraw, x, y, z) -> list[SolveReport]:
