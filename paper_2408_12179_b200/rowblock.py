@@ -228,12 +228,16 @@ class RowBlockGroup:
     def synchronize(self):
         self.stream.synchronize()
 
-    def owned_columns(self, local: int = 0) -> np.ndarray:
-        """Column indices owned by local rank ``local`` (hpr_group_col_layout)."""
+    def _col_layout(self):
+        """(K chunks, cw columns per rank and chunk, padded n) of hpr_group_col_layout."""
         k, cw, npad = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
         N.call("hpr_group_col_layout", self.g, ctypes.byref(k), ctypes.byref(cw),
                ctypes.byref(npad))
-        k, cw = int(k.value), int(cw.value)
+        return int(k.value), int(cw.value), int(npad.value)
+
+    def owned_columns(self, local: int = 0) -> np.ndarray:
+        """Column indices owned by local rank ``local`` (hpr_group_col_layout)."""
+        k, cw, _ = self._col_layout()
         g = self.rank0 + local
         cols = (np.arange(k)[:, None] * (self.P * cw) + g * cw + np.arange(cw)[None, :]).ravel()
         return cols[cols < self.n]
@@ -251,19 +255,28 @@ class RowBlockGroup:
                 dist.all_gather_object(got, parts[0])
                 parts = got
             return np.concatenate(parts)
+        # owned columns of rank g = slab g of every chunk: a (K, P, cw) view of
+        # the padded vector, so the pieces move by strided copies, not fancy indexing
+        k, cw, _ = self._col_layout()
+        if self.P == 1:
+            return self.blocks[0].to_host(name, slot)
         pieces = []
         for l, b in enumerate(self.blocks):
-            cols = self.owned_columns(l)
-            pieces.append((cols, b.to_host(name, slot)[cols]))
-        if self.nccl and self.P > 1:
+            pad = np.zeros(k * self.P * cw)
+            v = b.to_host(name, slot)
+            pad[:v.size] = v
+            g = self.rank0 + l
+            pieces.append((g, pad.reshape(k, self.P, cw)[:, g, :].copy()))
+        if self.nccl:
             import torch.distributed as dist
             got = [None] * self.P
             dist.all_gather_object(got, pieces[0])
             pieces = got
-        out = np.empty(self.n)
-        for cols, vals in pieces:
-            out[cols] = vals
-        return out
+        out = np.empty(k * self.P * cw)
+        slabs = out.reshape(k, self.P, cw)
+        for g, vals in pieces:
+            slabs[:, g, :] = vals
+        return out[:self.n]
 
     def close(self):
         if self.g is not None and self.g.value:
