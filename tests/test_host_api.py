@@ -178,3 +178,31 @@ class TestProblemTypes:
         ro, ci, v, m, n, m1 = stacked_arrays(p)
         assert (m, n, m1) == (2, 2, 1) and ro.tolist() == [0, 2, 3]
         assert ci.tolist() == [0, 1, 0] and v.tolist() == [1.0, 2.0, 3.0]
+
+
+@pytest.mark.parametrize("loop", ["0", "1"])
+def test_packed_batch_staging_layout(loop, monkeypatch):
+    """Packing into a staging buffer (solve_batch's path) gives the same arrays
+    as fresh packing, at the 256-byte-aligned upload layout BatchRun uses."""
+    import numpy as np
+    from paper_2408_12179_b200 import generate_known_solution_lp
+    from paper_2408_12179_b200.batch import PackedBatch
+    monkeypatch.setenv("HPR_PACK_LOOP", loop)
+    probs = [generate_known_solution_lp(s, 20 + s, 30 + 2 * s, 90 + 5 * s, 0.3)[0] for s in range(5)]
+    ref = PackedBatch(probs)
+    bufs = []
+
+    def staging(nb):
+        bufs.append(np.full(nb + 512, 0xAB, np.uint8))
+        return bufs[-1]
+
+    pk = PackedBatch(probs, staging=staging)
+    base = bufs[0].ctypes.data
+    off = 0
+    for name, dt in PackedBatch.ORDER:
+        a = pk.arrays[name]
+        assert a.dtype == np.dtype(dt)
+        assert a.ctypes.data == base + off
+        assert np.array_equal(a, ref.arrays[name].astype(dt))
+        off += (a.nbytes + 255) // 256 * 256
+    assert list(pk.arrays) == [k for k, _ in PackedBatch.ORDER]
