@@ -2,37 +2,48 @@
 """Benchmark of the HPR-LP iteration loop on B200 (contract: DESIGN.md §6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1|c3|c3-lite|c4|c5]
+                    [--config auto|c1|c2|c3|c3-lite|c4|c5]
 
-c1/c2/c3 (default c2 = BASELINE configs[1], the headline): a step is one full
-solve to tolerance (C2: 1e-8) from a problem already resident in HBM (setup =
-transpose/layout, scaling and power method are inside the step).  ``value`` =
-HPR iterations per second; at N > 1 every rank solves its own replica
-(independent objects, no collective: C2 fits one GPU) -- weak scaling.
+Default (``auto``): N = 1 runs C3 (BASELINE configs[2], the largest
+single-GPU configuration and the one the north-star target is quoted on);
+N > 1 runs C4, the row-block partitioned path.  ``--gpus N`` without a
+torchrun environment re-launches itself under ``torch.distributed.run`` with
+N ranks (127.0.0.1 rendezvous).
+
+c1/c2/c3: a step is one full solve to tolerance (C3: 1e-8) from a problem
+already resident in HBM; the step includes transpose/layout analysis,
+scaling, power method, all iterations and checkpoints.  ``value`` = HPR
+iterations per second (at N > 1 every rank solves its own replica: only with
+an explicit --config).
 
 c4: the row-block partitioned path: each rank owns
 ``--c4-rows`` rows x 100 nnz of a planted LP with n = 20M columns, generated
 per rank; the A^T y partials are reduce-scattered and w all-gathered over
 NCCL every iteration.  A step = one 150-iteration interval + checkpoint.
-Weak scaling (rows per rank fixed; N = 8 is C4's 1e9 nnz).
+Weak scaling: ``value`` = rank-block iterations per second (units all ranks
+processed / max-over-ranks time).  At N > 1 rank 0 also times the same block
+as a one-rank group (``one_rank``) so the efficiency is readable off one line.
 
 c5: a batch of 4096 LPs (m=500, n=1000, nnz=5000), one whole solve per CTA,
 sharded across ranks (no collective).  A step = the whole shard solved to
 1e-8.  ``value`` = LP-iterations per second summed over ranks.
 
 ``e2e`` = the same metric through the public API (``solve`` /
-``solve_batch`` / ``solve_distributed``) on host data, with the H2D upload and
-the D2H of the solution inside the timed region.  ``roofline`` is the fused
-x-phase + y-phase iteration pair against the measured HBM copy bandwidth,
-B_iter = 24 nnz + 4 (m + n + 2) + 8 (5 m + 8 n) bytes per iteration.
+``solve_batch`` / ``RowBlockGroup`` + ``solve``) on host data, with the H2D
+upload and the D2H of the solution inside the timed region.  ``roofline`` is
+the fused x-phase + y-phase iteration pair against the measured HBM copy
+bandwidth, B_iter = 24 nnz + 4 (m + n + 2) + 8 (5 m + 8 n) bytes per
+iteration, timed by CUDA events on the solver stream around every
+150-iteration graph replay.
 
-``--impl reference`` times the CPU oracle port (oracle/: the reference
-algorithm with sequential-order C kernels; OpenMP over all host cores, or a
-process pool for c5) on the same instance -- the reference is pure Python, so
-there is no compiled oracle/_ref.
+``--impl reference`` times the reference's own CPU solver (``hprlp`` installed
+in baseline/_ref, through its public functions: ``scale_problem``,
+``power_method_lambda_max``, ``run_inner`` / ``solve``) on the box's host cores,
+on the same instance; a step is a bounded sample of the workload (C1 and C5:
+whole solves; C2: 30 iterations; C3: 2 iterations; setup untimed).  Without
+baseline/_ref, or for C4 (beyond the reference's memory/time), it times the
+oracle port (oracle/: sequential-order C kernels, OpenMP over all host cores).
 """
-
-from __future__ import annotations
 
 import argparse
 import json
@@ -274,49 +285,204 @@ def c5_cpu_sample(count):
                       f"process, {min(cores, count)} processes), wall time incl. setup"}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The reference package (``hprlp``) installed in baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hprlp")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import hprlp
+        return hprlp
+    except Exception:
+        return None
+
+
+def to_reference_problem(hprlp, prob):
+    """The same instance as the reference's own ``LpProblem`` (its validation runs)."""
+    from hprlp.sparse import SparseMatrix as RefSparse
+
+    def block(a):
+        return RefSparse(np.asarray(a.row_offsets, np.int64), np.asarray(a.col_indices, np.int64),
+                         np.asarray(a.values, np.float64), int(a.nrows), int(a.ncols))
+    return hprlp.LpProblem(a_eq=block(prob.a_eq), a_ineq=block(prob.a_ineq),
+                           b_eq=np.asarray(prob.b_eq, np.float64),
+                           b_ineq=np.asarray(prob.b_ineq, np.float64),
+                           c=np.asarray(prob.c, np.float64),
+                           lower=np.asarray(prob.lower, np.float64),
+                           upper=np.asarray(prob.upper, np.float64),
+                           objective_constant=float(getattr(prob, "objective_constant", 0.0)),
+                           objective_negated=bool(getattr(prob, "objective_negated", False)))
+
+
+def host_info():
+    import platform
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": cpu_threads(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+# iterations per timed step of the reference's inner loop (a bounded sample:
+# C2 ~29 ms / C3 ~0.75 s per iteration on one core)
+REF_STEP_ITERS = {"c2": 30, "c3": 2, "c3-lite": 150}
+
+
+_C5_REF = []     # reference-shaped C5 LPs, built before the pool forks
+
+
+def _ref_c5_worker(i):
+    hprlp = import_reference()
+    rp = _C5_REF[i]
+    t0 = time.perf_counter()
+    rep = hprlp.solve(rp, hprlp.SolverConfig(tolerance=1e-8))
+    return rep.iterations, time.perf_counter() - t0
+
+
 def run_reference(args):
+    """The CPU reference arm: rank 0 only (other torchrun ranks exit at once)."""
     ws, rank, _ = dist_env()
+    ws = max(ws, args.gpus)
     if rank != 0:
         return
+    config = resolve_config(args.config, ws)
+    hprlp = import_reference() if config != "c4" else None
     base = {"metric": "hpr_iterations_per_sec", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference"}
-    if args.config == "c5":
-        cnt = max(cpu_threads(), 16)
-        vals = []
-        for _ in range(args.steps):
-            vals.append(c5_cpu_sample(cnt))
-        val = statistics.median(v["value"] for v in vals)
-        cb = dict(vals[0], value=val)
-        line = dict(base, metric="hpr_lp_iterations_per_sec", value=val, unit="LP-it/s",
-                    ms_per_step=None,
-                    config={"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
-                            "step": cb["sample"]},
-                    cpu_baseline=cb,
-                    e2e={"value": val, "unit": "LP-it/s", "h2d_bytes_per_step": 0,
-                         "d2h_bytes_per_step": 0})
+
+    def emit(line):
+        e = {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+             "d2h_bytes_per_step": 0}
+        line["e2e"] = e
+        line["cpu_baseline"] = dict(line["cpu_baseline"], value=line["value"])
+        line["config"]["host"] = host_info()
         print(json.dumps(line), flush=True)
+
+    if config == "c5":
+        import multiprocessing as mp
+        cores = cpu_threads()
+        cnt = max(cores, 16) * 4
+        pool_fn = _ref_c5_worker if hprlp is not None else _c5_worker
+        if hprlp is not None:
+            _C5_REF[:] = [to_reference_problem(hprlp, p) for p in c5_problems(0, cnt)]
+        kind = "reference" if hprlp is not None else "port"
+        ctx = mp.get_context("fork")
+        vals = []
+        with ctx.Pool(min(cores, cnt)) as pool:
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                out = pool.map(pool_fn, range(cnt))
+                dt = time.perf_counter() - t0
+                if i >= args.warmup:
+                    vals.append((sum(o[0] for o in out), dt))
+        val = sum(v[0] for v in vals) / sum(v[1] for v in vals)
+        who = "hprlp.solve (baseline/_ref)" if hprlp is not None else "the oracle port"
+        emit(dict(base, metric="hpr_lp_iterations_per_sec", value=val, unit="LP-it/s",
+                  ms_per_step=1e3 * sum(v[1] for v in vals) / len(vals),
+                  config={"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
+                          "step": f"{cnt} of the 4096 C5 LPs solved to 1e-8 by {who}, "
+                                  f"one LP per process, {min(cores, cnt)} processes"},
+                  cpu_baseline={"unit": "LP-it/s", "cores": min(cores, cnt), "kind": kind,
+                                "sample": f"{args.steps} x {cnt} whole LP solves"}))
         return
-    if args.config == "c4":
+
+    if config == "c4":
         from paper_2408_12179_b200.generators import generate_planted_block
         rows = args.c4_rows
         m1 = rows // 2
-        rp, ci, va, b, ys, m1l, (lo, up, xs, zs), cpart = generate_planted_block(
+        rp_, ci, va, b, ys, m1l, (lo, up, xs, zs), cpart = generate_planted_block(
             4, m1, rows - m1, C4_N, C4_PER_ROW, 0, rows)
-        prob = c4_lp((rp, ci, va, m1l, b, cpart + zs, lo, up), rows, m1)
-        interval = 2
-        tol = 1e-8
-        power_max = 3          # per-iteration time does not depend on lambda's accuracy
-    else:
-        prob, tol = make_instance(args.config)
-        interval = 150
-        power_max = 5000
-    O, scaled, st, threads = _oracle_setup(prob, power_max)
+        prob = c4_lp((rp_, ci, va, m1l, b, cpart + zs, lo, up), rows, m1)
+        O, scaled, st, threads = _oracle_setup(prob, 3)
+        for _ in range(args.warmup):
+            O.iterate_once(st, scaled)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            O.iterate_once(st, scaled)
+        dt = time.perf_counter() - t0
+        block_its = args.steps / dt
+        # one job iteration = ws rank blocks: the whole-job rate in the same
+        # unit as our arm (rank-block iterations per second) is the block rate
+        emit(dict(base, value=block_its, unit="rank-it/s", ms_per_step=1e3 * dt / args.steps,
+                  config={"workload": CONFIG_NAMES["c4"], "tolerance": 1e-8,
+                          "rows_per_rank": rows,
+                          "step": "1 HPR iteration over one rank block (oracle port; the "
+                                  "reference cannot hold C4)"},
+                  cpu_baseline={"unit": "rank-it/s", "cores": threads, "kind": "port",
+                                "sample": f"{args.steps} iterations of one 1.25M-row block"}))
+        return
+
+    prob, tol = make_instance(config)
+    if hprlp is not None:
+        from hprlp.core import ProblemData, SolverState, Variant as RefVariant, run_inner
+        from hprlp.scaling import scale_problem
+        from hprlp.sparse import power_method_lambda_max
+        rp = to_reference_problem(hprlp, prob)
+        del prob
+        if config == "c1":
+            # the same unit as our arm: one whole solve per step
+            cfg = hprlp.SolverConfig(tolerance=tol)
+            for _ in range(args.warmup):
+                hprlp.solve(rp, cfg)
+            its, dt, wall = 0, 0.0, 0.0
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                rep = hprlp.solve(rp, cfg)
+                wall += time.perf_counter() - t0
+                its += rep.iterations
+            val = its / wall
+            emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * wall / args.steps,
+                      config={"workload": CONFIG_NAMES[config], "tolerance": tol,
+                              "step": "one full hprlp.solve to tolerance (same unit as ours)",
+                              "status": rep.status.value, "iterations_per_solve": rep.iterations},
+                      cpu_baseline={"unit": "it/s", "cores": 1, "kind": "reference",
+                                    "sample": f"{args.steps} whole solves"}))
+            return
+        t0 = time.perf_counter()
+        scaled, _info = scale_problem(rp, ruiz_iters=10, pock_chambolle=True, bc_normalize=True)
+        data = ProblemData.from_problem(scaled)
+        t_scale = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        est = power_method_lambda_max(data.a, tol=1e-4, max_iters=5000)
+        t_power = time.perf_counter() - t0
+        state = SolverState.origin(data, sigma=1.0, lam=est.value, variant=RefVariant.HPR)
+        s = REF_STEP_ITERS.get(config, 150)
+        for _ in range(args.warmup):
+            run_inner(state, data, s)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run_inner(state, data, s)
+        dt = time.perf_counter() - t0
+        val = s * args.steps / dt
+        emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
+                  config={"workload": CONFIG_NAMES[config], "tolerance": tol,
+                          "step": f"{s} HPR iterations of the reference's run_inner "
+                                  "(hprlp from baseline/_ref, its own scipy/numpy path)",
+                          "setup_untimed_s": {"scale_problem": t_scale,
+                                              "power_method": t_power,
+                                              "power_iterations": est.iterations}},
+                  cpu_baseline={"unit": "it/s", "cores": 1, "kind": "reference",
+                                "sample": f"{args.steps} x {s} iterations after the "
+                                          "reference's own setup (single-threaded scipy SpMV)"}))
+        return
+
+    # no baseline/_ref: the oracle port on all host threads
+    O, scaled, st, threads = _oracle_setup(prob)
+    interval = 150 if config != "c3" else 10
 
     def step():
         for _ in range(interval):
             O.iterate_once(st, scaled)
-        O.half_step(st, scaled)
 
     for _ in range(args.warmup):
         step()
@@ -325,14 +491,11 @@ def run_reference(args):
         step()
     dt = time.perf_counter() - t0
     val = interval * args.steps / dt
-    line = dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
-                config={"workload": CONFIG_NAMES[args.config], "tolerance": tol,
-                        "step": f"{interval} HPR iterations + 1 half step (oracle port)"},
-                cpu_baseline={"value": val, "unit": "it/s", "cores": threads, "kind": "port",
-                              "sample": f"{args.steps} x {interval} iterations + half step"},
-                e2e={"value": val, "unit": "it/s", "h2d_bytes_per_step": 0,
-                     "d2h_bytes_per_step": 0})
-    print(json.dumps(line), flush=True)
+    emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
+              config={"workload": CONFIG_NAMES[config], "tolerance": tol,
+                      "step": f"{interval} HPR iterations (oracle port; baseline/_ref absent)"},
+              cpu_baseline={"unit": "it/s", "cores": threads, "kind": "port",
+                            "sample": f"{args.steps} x {interval} iterations"}))
 
 
 # ---------------------------------------------------------------------------
@@ -373,14 +536,15 @@ def run_ours(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = _dist_init(ws, local)
-    if args.config == "c5":
+    config = resolve_config(args.config, ws)
+    if config == "c5":
         return run_c5(args, dist, ws, rank, local)
-    if args.config == "c4":
+    if config == "c4":
         return run_c4(args, dist, ws, rank, local)
     import paper_2408_12179_b200 as P
     from paper_2408_12179_b200.device import DeviceLP
 
-    prob, tol = make_instance(args.config)
+    prob, tol = make_instance(config)
     cfg = P.SolverConfig(tolerance=tol)
     dev = DeviceLP(prob, device=local)
     m, n, nnz = dev.m, dev.n, dev.nnz
@@ -404,17 +568,18 @@ def run_ours(args):
     barrier()
     with sample_clocks:
         for _ in range(args.steps):
-            flush.zero_()
+            flush.zero_()                    # L2 flush on the default stream ...
+            torch.cuda.synchronize()         # ... finished before the step starts
+            dev.analyzed = False             # the step re-runs transpose + layout analysis
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
-            dev.stream.synchronize()
             ev0.record(dev.stream)
             rep = P.solve(prob, cfg, dev=dev)
             ev1.record(dev.stream)
             ev1.synchronize()
             total_ms += ev0.elapsed_time(ev1)
             its_total += rep.iterations
-            iter_s_total += rep.timings.iteration_seconds
+            iter_s_total += rep.device_stats["device_iteration_seconds"]
             reps.append(rep)
     barrier()
     launches = dev.launch_count() - l0
@@ -426,8 +591,11 @@ def run_ours(args):
     # solution back; one untimed call first warms the device-residency pool
     e2e_its, e2e_t = 0, 0.0
     h2d = d2h = 0
+    dev.close()
+    del dev
     P.solve(prob, cfg, device=local)
-    for _ in range(max(1, min(args.steps, 3))):
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(e2e_steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rep = P.solve(prob, cfg, device=local)
@@ -447,13 +615,21 @@ def run_ours(args):
         r0 = reps[-1]
         lay = r0.device_stats.get("layout", {})
         cpu = cpu_baseline_sample(prob) if ws == 1 and not args.no_cpu else None
+        if cpu is not None:
+            cpu["host"] = host_info()
         line = {
             "metric": "hpr_iterations_per_sec", "value": value, "unit": "it/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "tolerance": tol, "m": m, "n": n,
-                       "nnz": nnz, "step": "one full solve to tolerance from HBM-resident input",
+            "config": {"workload": CONFIG_NAMES[config], "tolerance": tol, "m": m, "n": n,
+                       "nnz": nnz,
+                       "step": "one full solve to tolerance from HBM-resident input "
+                               "(transpose/layout analysis, scaling, power method, "
+                               "iterations, checkpoints)",
+                       "e2e_step": "solve(problem) on host arrays: pinned H2D upload, setup, "
+                                   "solve, D2H of x, y, z",
+                       "e2e_steps": e2e_steps,
                        "status": r0.status.value, "iterations_per_solve": r0.iterations,
                        "wall_time_to_tol_s": t_max / args.steps,
                        "l2": "256 MB buffer written between timed steps (flush)",
@@ -461,16 +637,17 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": args.traffic if args.traffic is not None
-                         else load_traffic(args.config),
+                         else load_traffic(config),
                          "kernel": iteration_kernels(lay),
                          "bytes_per_iteration": bi, "peak_source": peak_kind,
-                         "timing": "CUDA events around each 150-iteration graph replay"},
+                         "timing": "CUDA events on the solver stream around each "
+                                   "150-iteration graph replay (the two iteration kernels)"},
             # the bound that actually binds a small-n problem (C2): every nonzero
             # is one random 8-byte operand gather = one L1TEX wavefront per cycle per SM
             # (phases on the staged engine gather from shared memory instead)
             "roofline_gather": gather_roofline(nnz, its_total, iter_s_total, lay),
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_val, "unit": "rank-it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": sample_clocks.summary(),
@@ -589,6 +766,38 @@ def c4_cpu_sample(block, m, m1, iters=6):
                       f"OpenMP {threads} threads), setup excluded"}
 
 
+def c4_one_rank(block, rows, local, steps, warmup):
+    """Rank 0's block solved by a one-rank group (NCCL world of 1): rank-it/s."""
+    import torch
+    from paper_2408_12179_b200.driver import LAMBDA_SAFETY
+    from paper_2408_12179_b200.rowblock import RowBlockGroup, nccl_unique_id
+    rp, ci, va, m1l, b, c, lo, up = block
+    grp = RowBlockGroup.distributed(block, n=C4_N, m_total=rows, m1_total=m1l,
+                                    nnz_total=int(rp[-1]), row0=0, rank=0, world=1,
+                                    nccl_id=nccl_unique_id(), device=local)
+    try:
+        grp.analyze()
+        grp.scale(10, True, True)
+        lam = grp.power(1e-4, 5000).raw * (1.0 + LAMBDA_SAFETY)
+        grp.state_reset()
+        k = 0
+        for i in range(warmup + steps):
+            if i == warmup:
+                torch.cuda.synchronize()
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(grp.stream)
+            grp.run_inner(150, k, k, 1.0, lam, 2)
+            grp.checkpoint(1.0, lam, 1, 0)
+            k += 150
+        ev1.record(grp.stream)
+        ev1.synchronize()
+        return {"value": 150 * steps / (ev0.elapsed_time(ev1) / 1e3), "unit": "rank-it/s",
+                "what": "rank 0's block as a one-rank group on one GPU, same step"}
+    finally:
+        grp.close()
+
+
 def run_c4(args, dist, ws, rank, local):
     import torch
     import paper_2408_12179_b200 as P
@@ -635,9 +844,23 @@ def run_c4(args, dist, ws, rank, local):
     launches = grp.launch_count() - l0
     t_max, _ = _max_sum(dist, local, t_local, 0)
     its = interval * args.steps
-    value = its / t_max               # every rank advances the same iterations
+    # units all ranks processed / max-over-ranks time: every job iteration
+    # advances each of the ws rank blocks once (weak scaling)
+    value = ws * its / t_max
     nnz_rank = rows * C4_PER_ROW
+    comm = grp.comm_info() if hasattr(grp, "comm_info") else None
     grp.close()
+
+    one_rank = None
+    if ws > 1:
+        # the same per-rank block as a one-rank group on rank 0's GPU (the other
+        # GPUs idle at the barrier): the denominator of the weak-scaling efficiency
+        if dist is not None:
+            dist.barrier()
+        if rank == 0:
+            one_rank = c4_one_rank(block, rows, local, args.steps, args.warmup)
+        if dist is not None:
+            dist.barrier()
 
     # e2e through the public API from this rank's host block: every step
     # uploads the block (pinned staging -> H2D), builds the rank group and runs
@@ -665,20 +888,25 @@ def run_c4(args, dist, ws, rank, local):
         finally:
             g2.close()
     t_e2e, _ = _max_sum(dist, local, e2e_t, 0)
-    e2e_val = e2e_its / t_e2e
+    e2e_val = ws * e2e_its / t_e2e
     peak, peak_kind = load_peaks()
     bi_rank = b_iter(rows, C4_N, nnz_rank)
     achieved = bi_rank * its / inner_s / 1e9
     line = None
     if rank == 0:
         line = {
-            "metric": "hpr_iterations_per_sec", "value": value, "unit": "it/s", "n_gpus": ws,
+            "metric": "hpr_iterations_per_sec", "value": value, "unit": "rank-it/s",
+            "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": CONFIG_NAMES["c4"], "m": m, "n": C4_N,
                        "nnz": m * C4_PER_ROW, "rows_per_rank": rows,
                        "step": "150 HPR iterations + checkpoint (row-block, NCCL RS/AG per iteration)",
+                       "job_iterations_per_sec": its / t_max,
+                       "unit_note": "rank-it/s = job iterations/s x ranks (each job iteration "
+                                    "advances every rank's 1.25M-row block once)",
+                       "one_rank": one_rank, "nccl": comm,
                        "lambda": lam, "power_iterations": est.iterations,
                        "l2": "working set > L2 (no flush needed)",
                        "parallelism": f"row-block x{ws} (NCCL)"},
@@ -698,24 +926,88 @@ def run_c4(args, dist, ws, rank, local):
     return line
 
 
+def resolve_config(config: str, ws: int) -> str:
+    """``auto``: C3 on one GPU (the headline), the row-block C4 path on N > 1."""
+    if config == "auto":
+        return "c3" if ws <= 1 else "c4"
+    return config
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(argv, nproc: int) -> int:
+    """Re-run this script under torch.distributed.run with ``nproc`` ranks
+    (one per GPU, 127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_ALGO", "Ring")       # fixed reduction order at a given N
+    env.setdefault("NCCL_PROTO", "Simple")
+    env.setdefault("NCCL_DEBUG", "INFO")      # communicator init lines show nranks
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args):
+    """Launch check without a GPU: every rank joins a gloo group, the ranks
+    are summed, rank 0 prints what it saw."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([1, rank], dtype=torch.int64)
+    if ws > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "world_size": ws, "ranks_joined": int(t[0]),
+                          "rank_sum": int(t[1]), "config": resolve_config(args.config, ws),
+                          "NCCL_ALGO": os.environ.get("NCCL_ALGO"),
+                          "NCCL_PROTO": os.environ.get("NCCL_PROTO")}), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=tuple(CONFIG_NAMES), default="c2")
+    ap.add_argument("--config", choices=("auto",) + tuple(CONFIG_NAMES), default="auto")
     ap.add_argument("--c4-rows", type=int, default=1_250_000,
                     help="rows per rank of the c4 weak-scaling instance (100 nnz each)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu DRAM bytes per iteration of the kernel pair (from profiles/)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch check only (gloo, no GPU work)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (
+            args.impl == "ours" or args.dry_run):
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
+        ws = dist_env()[0]
+        if args.gpus != ws:
+            ap.error(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
+        if ws > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         run_ours(args)
 
 

@@ -275,6 +275,9 @@ int hpr_group_kkt(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out);
 int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *out);
 int hpr_group_last_times(hpr_group *g, double *inner_ms, double *ckpt_ms);
 int hpr_group_launch_count(hpr_group *g, int64_t *count);
+/* transport (1 = NCCL, 0 = local kernels), and -- from the NCCL communicator
+ * itself when NCCL is used -- its rank count, this rank and the NCCL version */
+int hpr_group_comm_info(hpr_group *g, int *transport, int *nranks, int *rank, int *version);
 
 /* ------------------------------------------------------------------------
  * Batch of small LPs (BASELINE config C5; csrc/hpr_batch.cuh): one whole

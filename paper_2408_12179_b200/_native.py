@@ -184,6 +184,7 @@ _SIGS = {
     "hpr_group_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_double)]),
     "hpr_group_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "hpr_group_comm_info": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_int)] * 4),
     # batch of small LPs (hpr_batch.cuh)
     "hpr_batch_smem_bytes": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_size_t)]),

@@ -27,7 +27,7 @@ _STATUS = {0: SolveStatus.OPTIMAL, 1: SolveStatus.ITERATION_LIMIT, 2: SolveStatu
            3: SolveStatus.NUMERICAL_ERROR}
 _TRIGGER = {0: "sufficient", 1: "stalled", 2: "long_loop"}
 _VARIANT = {Variant.DR: 0, Variant.HDR_FIXED_SIGMA: 1, Variant.HDR: 2, Variant.HPR: 3}
-MAX_LOG = 64
+MAX_LOG = 64       # restart records kept per LP in the first pass (solve_batch re-runs overflows)
 
 
 def _torch():
@@ -201,8 +201,10 @@ def _batch_stream(torch, device):
 class BatchRun:
     """Device residency of one packed batch + its native solve (re-runnable)."""
 
-    def __init__(self, packed: PackedBatch, device: int = 0, stream=None, pinned: bool = True):
+    def __init__(self, packed: PackedBatch, device: int = 0, stream=None, pinned: bool = True,
+                 max_log: int = MAX_LOG):
         torch = _torch()
+        self.max_log = int(max_log)
         if not torch.cuda.is_available():
             raise N.NativeUnavailableError("CUDA device required: the batch path has no CPU fallback")
         N.load_library()
@@ -258,12 +260,12 @@ class BatchRun:
             self.y = torch.empty(max(pb.total_rows, 1), **f64)
             self.res = torch.empty(packed.count * ctypes.sizeof(N.HprBatchResult),
                                    dtype=torch.uint8, device=self.device)
-            self.log = torch.empty(packed.count * MAX_LOG * ctypes.sizeof(N.HprRestartRec),
+            self.log = torch.empty(packed.count * self.max_log * ctypes.sizeof(N.HprRestartRec),
                                    dtype=torch.uint8, device=self.device)
         self.launches = 0
 
     def launch(self, cfg: SolverConfig):
-        c = _config(cfg, MAX_LOG)
+        c = _config(cfg, self.max_log)
         N.call("hpr_batch_solve", ctypes.byref(self.pb), ctypes.byref(c),
                ctypes.c_void_p(self.ws.data_ptr()), ctypes.c_size_t(self.ws.numel()),
                ctypes.c_void_p(self.res.data_ptr()), ctypes.c_void_p(self.log.data_ptr()),
@@ -281,20 +283,27 @@ class BatchRun:
         gc.disable()
         try:
             return _build_reports(self.packed, self.res.cpu().numpy(), self.log.cpu().numpy(),
-                                  self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy())
+                                  self.x.cpu().numpy(), self.y.cpu().numpy(), self.z.cpu().numpy(),
+                                  self.max_log)
         finally:
             if was:
                 gc.enable()
 
 
-def _build_reports(pk: PackedBatch, raw, lraw, x, y, z) -> list[SolveReport]:
+class RestartLogOverflow(RuntimeWarning):
+    """A batch LP restarted more often than its restart-log capacity: its
+    report's ``restart_log`` is truncated (``solve_batch`` re-runs such LPs
+    with a log large enough, so its reports are always complete)."""
+
+
+def _build_reports(pk: PackedBatch, raw, lraw, x, y, z, max_log: int = MAX_LOG) -> list[SolveReport]:
     """SolveReports of a batch from the device result records (column-wise
     numpy views of the C structs; the solution arrays are views of fresh host
     copies of the batch vectors)."""
     rs = np.frombuffer(np.ascontiguousarray(raw).tobytes(), dtype=np.dtype(N.HprBatchResult),
                        count=pk.count)
     recs = np.frombuffer(np.ascontiguousarray(lraw).tobytes(), dtype=np.dtype(N.HprRestartRec),
-                         count=pk.count * MAX_LOG).reshape(pk.count, MAX_LOG)
+                         count=pk.count * max_log).reshape(pk.count, max_log)
     col = {f: rs[f].tolist() for f in rs.dtype.names if f != "kkt"}
     kkts = rs["kkt"].tolist()
     if any(p and not c for p, c in zip(col["power_iterations"], col["power_converged"])):
@@ -307,7 +316,11 @@ def _build_reports(pk: PackedBatch, raw, lraw, x, y, z) -> list[SolveReport]:
             warnings.warn("negative quadratic form in the merit: lambda may underestimate "
                           "lambda_1(AA*)", RuntimeWarning)
     ro, co = pk.row_off.tolist(), pk.col_off.tolist()
-    nlog = [min(v, MAX_LOG) for v in col["n_log"]]
+    over = sum(1 for v in col["n_log"] if v > max_log)
+    if over:
+        warnings.warn(f"{over} LP(s) restarted more than {max_log} times: restart_log truncated",
+                      RestartLogOverflow)
+    nlog = [min(v, max_log) for v in col["n_log"]]
     lmax = max(nlog) if nlog else 0
     rec_cols = {f: recs[f][:, :lmax].tolist() for f in recs.dtype.names}
     out = []
@@ -348,7 +361,23 @@ def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
         run = BatchRun(packed, device=device)
         packed.arrays = {}                        # views of the staging buffer: released
     run.launch(cfg)
-    return run.reports(cfg)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RestartLogOverflow)
+        reps = run.reports(cfg)
+    over = [i for i, r in enumerate(reps) if r.restarts > len(r.restart_log)]
+    if over:
+        # the reference logs every restart: re-solve the LPs whose log overflowed
+        # with room for all of them (each CTA's solve is deterministic and
+        # independent of the rest of the batch, so the results are identical)
+        need = max(reps[i].restarts for i in over)
+        with _Staging.lock:
+            sub = PackedBatch([problems[i] for i in over])
+        rerun = BatchRun(sub, device=device, max_log=need)
+        rerun.launch(cfg)
+        for i, r in zip(over, rerun.reports(cfg)):
+            r.device_stats["batch_index"] = i
+            reps[i] = r
+    return reps
 
 
 def shard_bounds(count: int, world: int, rank: int) -> tuple[int, int]:

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -74,6 +75,25 @@ enum {
   R_NUP, R_CLAMP, R_R2, R_SH2, R_ATY2, R_SUMSQ0, R_SUMSQ1, R_SUMSQ2, R_SUMSQ3, R_POW_U2, R_NONFIN, R_POW_VW,
   R_POW_WW, R_COUNT
 };
+
+// Function attributes are per device, and concurrent solves may launch from
+// several host threads: the configured dynamic shared memory (and the SELL
+// kernels' occupancy) is remembered per (kernel, device) under a mutex.
+std::mutex g_attr_mu;
+std::map<std::pair<const void *, int>, int> g_attr;
+
+template <class K>
+int ensure_dyn_smem(K kern, int bytes) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int &have = g_attr[{(const void *)kern, dev}];
+  if (bytes > have) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+  }
+  return 0;
+}
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -420,14 +440,20 @@ namespace {
 template <int U, bool GA, class Epi>
 int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
                   int *grid_out, bool pdl) {
-  static int occ = 0;
-  if (occ == 0) {
-    if (HPR_CARVEOUT >= 0)   // shared-memory carve-out: 0 = the whole unified array as L1
-      CK(cudaFuncSetAttribute(k_sell<U, GA, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              HPR_CARVEOUT));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<U, GA, Epi>, kThreads, 0));
-    if (occ < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
-    occ = std::min(occ, kMaxGridPerSm);
+  int occ = 0;
+  {
+    const void *kf = (const void *)k_sell<U, GA, Epi>;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int &o = g_attr[{kf, c->device}];
+    if (o == 0) {
+      if (HPR_CARVEOUT >= 0)   // shared-memory carve-out: 0 = the whole unified array as L1
+        CK(cudaFuncSetAttribute(k_sell<U, GA, Epi>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                HPR_CARVEOUT));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sell<U, GA, Epi>, kThreads, 0));
+      if (o < 1) return fail(HPR_ECUDA, "SELL kernel does not fit on an SM");
+      o = std::min(o, kMaxGridPerSm);
+    }
+    occ = o;
   }
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
@@ -640,11 +666,7 @@ int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *
 
 template <class Epi>
 int launch_stg(hpr_ctx *c, const hpr_ctx::Stg &T, int ncols, const double *xg, const Epi &epi) {
-  static int smem_set = 0;
-  if (T.smem > smem_set) {
-    CK(cudaFuncSetAttribute(k_stg<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, T.smem));
-    smem_set = T.smem;
-  }
+  if (int e = ensure_dyn_smem(k_stg<Epi>, T.smem)) return e;
   k_stg<Epi><<<T.G, kStgThreads, T.smem, c->stream>>>(c->stgmat(T, ncols), xg, epi);
   CKL();
   c->launches += 1;
@@ -840,11 +862,7 @@ int cb_layout(hpr_ctx *c, char *&p, hpr_ctx::Cb &C, const int *rp, const int *ci
 
 template <int RPT, class Epi>
 int launch_cb_r(hpr_ctx *c, const hpr_ctx::Cb &C, int ncols, const double *xg, const Epi &epi) {
-  static bool smem_set = false;
-  if (!smem_set) {
-    CK(cudaFuncSetAttribute(k_cb<RPT, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbMaxSmem));
-    smem_set = true;
-  }
+  if (int e = ensure_dyn_smem(k_cb<RPT, Epi>, kCbMaxSmem)) return e;
   k_cb<RPT, Epi><<<C.G, kCbThreads + 32, C.smem, c->stream>>>(c->cbmat(C, ncols), xg, epi, nullptr);
   CKL();
   c->launches += 1;

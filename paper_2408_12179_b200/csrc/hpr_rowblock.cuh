@@ -177,14 +177,21 @@ struct NcclApi {
   decltype(&ncclReduceScatter) reduceScatter = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
+  decltype(&ncclCommCount) commCount = nullptr;          // optional (diagnostics)
+  decltype(&ncclCommUserRank) commUserRank = nullptr;
+  decltype(&ncclGetVersion) getVersion = nullptr;
   bool ok = false;
 };
 
 NcclApi &nccl() {
   static NcclApi api;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Fixed reduction order run to run at a given P: ring reduce-scatter with
+    // the Simple protocol unless the caller pinned something else (NCCL reads
+    // these when a communicator is created).
+    setenv("NCCL_ALGO", "Ring", 0);
+    setenv("NCCL_PROTO", "Simple", 0);
     // prefer the copy already in the process (PyTorch's), else the loader's
     void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -198,10 +205,13 @@ NcclApi &nccl() {
       api.reduceScatter = (decltype(api.reduceScatter))dlsym(h, "ncclReduceScatter");
       api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
       api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+      api.commCount = (decltype(api.commCount))dlsym(h, "ncclCommCount");
+      api.commUserRank = (decltype(api.commUserRank))dlsym(h, "ncclCommUserRank");
+      api.getVersion = (decltype(api.getVersion))dlsym(h, "ncclGetVersion");
       api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce &&
                api.reduceScatter && api.allGather && api.errStr;
     }
-  }
+  });
   return api;
 }
 
@@ -1185,6 +1195,21 @@ int hpr_group_finalize(hpr_group *g, int term_original, int slot, hpr_ckpt_out *
 int hpr_group_last_times(hpr_group *g, double *inner_ms, double *ckpt_ms) {
   if (!g) return fail(HPR_EINVAL, "null group");
   return hpr_last_times(g->r[0].c, inner_ms, ckpt_ms);
+}
+
+int hpr_group_comm_info(hpr_group *g, int *transport, int *nranks, int *rank, int *version) {
+  if (!g || !transport || !nranks || !rank || !version) return fail(HPR_EINVAL, "null argument");
+  *transport = g->use_nccl ? 1 : 0;
+  *nranks = g->P;
+  *rank = g->rank0;
+  *version = 0;
+  if (g->use_nccl && g->comm) {
+    NcclApi &api = nccl();
+    if (api.commCount) NK(api.commCount(g->comm, nranks));
+    if (api.commUserRank) NK(api.commUserRank(g->comm, rank));
+    if (api.getVersion) NK(api.getVersion(version));
+  }
+  return HPR_OK;
 }
 
 int hpr_group_launch_count(hpr_group *g, int64_t *count) {

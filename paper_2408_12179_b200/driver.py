@@ -160,10 +160,15 @@ class RestartEvent:
 
 @dataclass
 class Timings:
-    """driver.py:130-151.  iteration / checkpoint seconds are CUDA-event device
-    times of the graph replays and checkpoint sequences; scaling_seconds covers
-    upload + transpose/tiling + scaling (excluded from solve_seconds, as the
-    reference excludes parsing and scaling); power_method_seconds is wall time."""
+    """driver.py:130-151, wall-clock like the reference's ``perf_counter``
+    stage boundaries (driver.py:292-372).  The inner graph replay and the
+    checkpoint share one host synchronisation, so an interval's wall time is
+    split with the checkpoint's device time: checkpoint_seconds = its CUDA-event
+    time + the host scalar logic, iteration_seconds = the rest of the interval.
+    scaling_seconds covers upload + transpose/tiling + scaling (excluded from
+    solve_seconds, as the reference excludes parsing and scaling).  The pure
+    device times are in ``SolveReport.device_stats`` (``device_iteration_seconds``,
+    ``device_checkpoint_seconds``)."""
 
     scaling_seconds: float = 0.0
     power_method_seconds: float = 0.0
@@ -360,6 +365,20 @@ def solve(problem, cfg=None, *, device: int = 0, dev: DeviceLP | None = None) ->
         DEVICE_POOL.release(dev)
 
 
+def _time_limit_hit(dev, wall_start: float, limit: float) -> bool:
+    """driver.py:345 (wall time since the solve started).  A row-block group
+    (one rank per process) must take the same branch on every rank -- one rank
+    finalizing (all-gather) while another runs the next interval
+    (reduce-scatter) would mismatch the collectives -- so the per-rank
+    decisions are OR-reduced over the group (``any_rank``).  Every rank holds
+    the same ``cfg``, so an infinite limit skips the collective everywhere."""
+    if not math.isfinite(limit):
+        return False
+    hit = time.perf_counter() - wall_start >= limit
+    agree = getattr(dev, "any_rank", None)
+    return bool(agree(hit)) if agree is not None else hit
+
+
 def _solve(problem, cfg, dev) -> SolveReport:
     cfg = SolverConfig.coerce(cfg)
     wall_start = time.perf_counter()
@@ -401,15 +420,20 @@ def _solve(problem, cfg, dev) -> SolveReport:
     good_slot = None       # candidate slot of the last completed checkpoint
     slot = 0
 
+    dev_it_s = dev_ck_s = 0.0
     while status is None:
         steps = min(cfg.check_interval, cfg.max_iterations - k)
         lamsig = lam * sigma
+        tw0 = time.perf_counter()
         if steps > 0:
             dev.run_inner(steps, t, k, sigma, lamsig, vcode)
         o = dev.checkpoint(sigma, lamsig, term_original, slot)   # one sync
+        tw1 = time.perf_counter()
         it_s, ck_s = dev.last_times()
-        timings.iteration_seconds += it_s if steps > 0 else 0.0
+        it_s = it_s if steps > 0 else 0.0
+        dev_it_s += it_s
         if o.nonfinite_k >= 0:
+            timings.iteration_seconds += tw1 - tw0
             # NumericalBreakdownError(k) inside run_inner: k is not advanced for
             # the failing step and no checkpoint of this interval counts.
             k = int(o.nonfinite_k)
@@ -417,7 +441,10 @@ def _solve(problem, cfg, dev) -> SolveReport:
             break
         t += max(steps, 0)
         k += max(steps, 0)
-        timings.checkpoint_seconds += ck_s
+        dev_ck_s += ck_s
+        ck_wall = min(ck_s, tw1 - tw0)
+        timings.iteration_seconds += (tw1 - tw0) - ck_wall
+        timings.checkpoint_seconds += ck_wall
         res = kkt_from_sums(o, bnorm, cnorm, objective_constant)
         good_slot = slot
         slot = 1 - slot
@@ -425,7 +452,7 @@ def _solve(problem, cfg, dev) -> SolveReport:
             status = SolveStatus.OPTIMAL
         elif k >= cfg.max_iterations:
             status = SolveStatus.ITERATION_LIMIT
-        elif time.perf_counter() - wall_start >= cfg.time_limit_seconds:
+        elif _time_limit_hit(dev, wall_start, cfg.time_limit_seconds):
             status = SolveStatus.TIME_LIMIT
         elif variant.uses_restarts:
             merit_now = merit_from_sums(o, sigma, lam)
@@ -448,6 +475,7 @@ def _solve(problem, cfg, dev) -> SolveReport:
                 merit_prev = math.inf
             else:
                 merit_prev = merit_now
+        timings.checkpoint_seconds += time.perf_counter() - tw1      # host scalar logic
 
     if good_slot is None:
         # breakdown before the first checkpoint: the origin (driver.py:374-380)
@@ -477,7 +505,8 @@ def _solve(problem, cfg, dev) -> SolveReport:
         device_stats={"lambda_raw": est.raw, "power_iterations": est.iterations,
                       "b_factor": sc.b_factor, "c_factor": sc.c_factor,
                       "launches": dev.launch_count() - launches0, "layout": layout,
-                      "h2d_bytes": dev.h2d_bytes})
+                      "h2d_bytes": dev.h2d_bytes, "device_iteration_seconds": dev_it_s,
+                      "device_checkpoint_seconds": dev_ck_s})
 
 
 def kkt_residual(problem, point: PrimalDualPoint, *, dev: DeviceLP | None = None,

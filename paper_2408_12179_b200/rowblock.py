@@ -228,6 +228,31 @@ class RowBlockGroup:
     def synchronize(self):
         self.stream.synchronize()
 
+    def comm_info(self) -> dict:
+        """Transport and, for NCCL, the communicator's own rank count / rank /
+        version (hpr_group_comm_info) plus the pinned algorithm / protocol."""
+        import os
+        if self.g is None:
+            return {"transport": "nccl" if self.nccl else "local", "nranks": self.P}
+        v = [ctypes.c_int(0) for _ in range(4)]
+        N.call("hpr_group_comm_info", self.g, *[ctypes.byref(x) for x in v])
+        tr, nr, rk, ver = (x.value for x in v)
+        return {"transport": "nccl" if tr else "local", "nranks": nr, "rank": rk,
+                "nccl_version": ver, "NCCL_ALGO": os.environ.get("NCCL_ALGO"),
+                "NCCL_PROTO": os.environ.get("NCCL_PROTO")}
+
+    def any_rank(self, flag: bool) -> bool:
+        """OR of ``flag`` over all ranks of the group (a MAX all-reduce over
+        torch.distributed in NCCL mode; the local transport is one process)."""
+        if not (self.nccl and self.P > 1):
+            return bool(flag)
+        import torch.distributed as dist
+        torch = _torch()
+        dev = self.blocks[0].device if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return bool(int(t.item()))
+
     def _col_layout(self):
         """(K chunks, cw columns per rank and chunk, padded n) of hpr_group_col_layout."""
         k, cw, npad = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
