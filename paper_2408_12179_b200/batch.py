@@ -202,9 +202,9 @@ class BatchRun:
     """Device residency of one packed batch + its native solve (re-runnable)."""
 
     def __init__(self, packed: PackedBatch, device: int = 0, stream=None, pinned: bool = True,
-                 max_log: int = MAX_LOG):
+                 max_log: int | None = None):
         torch = _torch()
-        self.max_log = int(max_log)
+        self.max_log = int(MAX_LOG if max_log is None else max_log)
         if not torch.cuda.is_available():
             raise N.NativeUnavailableError("CUDA device required: the batch path has no CPU fallback")
         N.load_library()

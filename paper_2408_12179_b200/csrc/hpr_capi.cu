@@ -344,6 +344,7 @@ struct Sell {
       *long_rows = nullptr, *nsel = nullptr;
   int *ci = nullptr, *pos = nullptr;
   double *val_s = nullptr, *val0 = nullptr;
+  bool affinity = false;   // rows in the row-affinity order (row_affinity_order)
 };
 
 }  // namespace
@@ -389,6 +390,10 @@ struct hpr_ctx {
   unsigned int *flags = nullptr;
   int bounds_uniform = 0;          // see EpiXIter
   int keep_a = 0, keep_at = 0;     // L2 policy of the A / A^T streams (SellMat::keep)
+  // persisting-L2 window on the dual iterate y (HPR_L2WIN): attached to the
+  // inner-loop SELL launches while they are captured (l2win_active)
+  bool l2win_active = false;
+  cudaAccessPolicyWindow l2win{};
   double lo_u = 0.0, up_u = 0.0;
   double *h_results = nullptr;       // pinned
   IterParams *h_params = nullptr;    // pinned
@@ -457,16 +462,23 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
   }
   const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
   const int grid = std::max(1, std::min(nwin, occ * c->num_sms));
-  if (pdl && HPR_PDL) {
+  if ((pdl && HPR_PDL) || c->l2win_active) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl && HPR_PDL) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (c->l2win_active) {
+      at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[na++].val.accessPolicyWindow = c->l2win;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelEx(&cfg, k_sell<U, GA, Epi>, M, xg, epi, part));
   } else {
     k_sell<U, GA, Epi><<<grid, kThreads, 0, c->stream>>>(M, xg, epi, part);
@@ -523,9 +535,52 @@ Parts parts_of(const hpr_ctx *c) {
 
 int sumsq_blocks(int64_t n) { return grid_for(n, kThreads, kSumsqBlocks); }
 
+// Row affinity order of a matrix whose gathered vector (ncols doubles) does
+// not fit in L2 (k_row_mode_block): rows stably radix-sorted by the column block
+// holding most of their entries.  Scratch: keys_out / row_of (nnz ints each,
+// free once the transpose is built); needs nnz >= 2 nrows.  Returns the order
+// (row_of + nrows) or nullptr when not used.  HPR_RAO (A) / HPR_RAO_AT (A^T)
+// = 0 / 1 force it off / on; HPR_RAO_BITS sets the block width (default 2^20
+// columns = 8 MB of the vector).
+const int *row_affinity_order(hpr_ctx *c, const int *rp, const int *ci, int nrows, int64_t ncols,
+                              bool transpose, int *rc) {
+  *rc = HPR_OK;
+  const char *env = getenv(transpose ? "HPR_RAO_AT" : "HPR_RAO");
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+  bool want = 8.0 * (double)ncols > (double)l2;
+  if (env && env[0] == '0') want = false;
+  if (env && env[0] == '1') want = true;
+  if (!want || nrows < 2 || c->d.nnz < 2 * (int64_t)nrows) return nullptr;
+  int bits = 20;   // C3 sweep (us/iteration): 12: 976, 14: 981, 16: 942, 18: 919, 20: 916, 22: 921, off: 946
+  if (const char *eb = getenv("HPR_RAO_BITS")) bits = std::max(0, std::min(30, atoi(eb)));
+  int *key = (int *)(c->ws + c->L.keys_out), *skey = key + nrows;
+  int *iota = (int *)(c->ws + c->L.row_of), *order = iota + nrows;
+  cudaStream_t s = c->stream;
+  k_row_mode_block<<<grid_for(nrows), 256, 0, s>>>(rp, ci, nrows, bits, key);
+  k_iota<<<grid_for(nrows), 256, 0, s>>>(iota, nrows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *rc = fail(HPR_ECUDA, std::string("row affinity: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  int end_bit = 1;
+  while (end_bit < 31 && (1LL << end_bit) <= ((ncols - 1) >> bits)) ++end_bit;
+  size_t tb = c->L.cub_bytes;
+  e = cub::DeviceRadixSort::SortPairs(c->ws + c->L.cub_tmp, tb, key, skey, iota, order, nrows, 0,
+                                      end_bit, s);
+  if (e != cudaSuccess) {
+    *rc = fail(HPR_ECUDA, std::string("row affinity sort: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  c->launches += 3;
+  return order;
+}
+
 // SELL plan of one matrix: slice order, slot offsets, long-row list
 int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
-              int long_thresh = kLongRow, int m_pad = 0, int m_real = 0) {
+              int long_thresh = kLongRow, int m_pad = 0, int m_real = 0,
+              const int *order = nullptr) {
   S.nrows = nrows;
   const int nw = (int)windows_of(nrows);
   S.nslices = nw * (kWindow / kSlice);
@@ -542,11 +597,12 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   if (win == kSortWinBig)
     k_sell_plan<kSortWinBig><<<(nrows + win - 1) / win, win, 0, s>>>(
         rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots, S.long_flag, long_thresh, m_pad,
-        m_real);
+        m_real, order);
   else
     k_sell_plan<kWindow><<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len,
                                                 S.slice_slots, S.long_flag, long_thresh, m_pad,
-                                                m_real);
+                                                m_real, order);
+  S.affinity = order != nullptr;
   CKL();
   size_t tb = c->L.cub_bytes;
   CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, S.slice_slots, S.slice_ptr,
@@ -1106,9 +1162,17 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
     CKL();
     c->launches += 1;
   }
-  rc = plan_sell(c, c->L.pa, B.a_rp, m, c->sa);
+  {
+    const int *order = row_affinity_order(c, B.a_rp, B.a_ci, m, n, false, &rc);
+    if (rc) return rc;
+    rc = plan_sell(c, c->L.pa, B.a_rp, m, c->sa, kLongRow, 0, 0, order);
+  }
   if (rc) return rc;
-  rc = plan_sell(c, c->L.pat, B.at_rp, n, c->sat);
+  {
+    const int *order = row_affinity_order(c, B.at_rp, B.at_ci, n, m, true, &rc);
+    if (rc) return rc;
+    rc = plan_sell(c, c->L.pat, B.at_rp, n, c->sat, kLongRow, 0, 0, order);
+  }
   if (rc) return rc;
   rc = cb_plan(c, c->L.ca, B.a_rp, B.a_ci, m, c->cba);
   if (rc) return rc;
@@ -1162,7 +1226,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   // structure), drop them otherwise
   std::vector<long long> sig = {(long long)(uintptr_t)layout, (long long)bytes};
   for (const Sell *S : {&c->sa, &c->sat, &c->sp.S})
-    for (long long v : {(long long)S->nslices, S->slots, (long long)S->nlong}) sig.push_back(v);
+    for (long long v : {(long long)S->nslices, S->slots, (long long)S->nlong, (long long)S->affinity})
+      sig.push_back(v);
   for (long long v : {(long long)c->sp.on, (long long)c->sp.NB, (long long)c->sp.W}) sig.push_back(v);
   for (const hpr_ctx::Stg *T : {&c->sta, &c->stat})
     for (long long v : {(long long)T->on, (long long)T->G, (long long)T->NB, (long long)T->rows_cap,
@@ -1450,6 +1515,36 @@ int hpr_state_reset(hpr_ctx *c) {
   return HPR_OK;
 }
 
+// Persisting-L2 window over y for the inner loop (HPR_L2WIN=1, opt-in): the
+// dual iterate is gathered by the x-phase (random segments) and streamed by
+// the y-phase; with a window it stays L2-resident while the matrix and the
+// n-vectors stream past it.  The device's persisting carve-out is raised to
+// the window (capped at the device maximum); hitRatio covers the remainder.
+int l2_window_setup(hpr_ctx *c) {
+  c->l2win_active = false;
+  const char *env = getenv("HPR_L2WIN");
+  if (!(env && env[0] == '1')) return HPR_OK;
+  int maxp = 0, maxw = 0;
+  CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device));
+  CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
+  if (maxp <= 0 || maxw <= 0) return HPR_OK;
+  const size_t ybytes = sizeof(double) * (size_t)c->d.m;
+  size_t limit = 0;
+  CK(cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize));
+  const size_t want = std::min(ybytes, (size_t)maxp);
+  if (limit < want) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  CK(cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize));
+  cudaAccessPolicyWindow w{};
+  w.base_ptr = (void *)c->B.y;
+  w.num_bytes = std::min(ybytes, (size_t)maxw);
+  w.hitRatio = (float)std::min(1.0, (double)limit / (double)w.num_bytes);
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
+  c->l2win = w;
+  c->l2win_active = true;
+  return HPR_OK;
+}
+
 int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, double lamsig,
                   int variant) {
   int rc = check_ctx(c, true, true);
@@ -1481,6 +1576,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     ey.m1 = (int)c->d.m1;
     cudaGraph_t g;
     const long long before = c->launches;
+    if (int e2 = l2_window_setup(c)) return e2;
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < steps; ++i) {
       ex.step = i;
@@ -1494,10 +1590,12 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
               : c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
                           : launch_a_iter(c, B.w, ey, true);
       if (rc2) {
+        c->l2win_active = false;
         cudaStreamEndCapture(s, &g);
         return rc2;
       }
     }
+    c->l2win_active = false;
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
     cudaGraphExec_t exe;
@@ -1656,6 +1754,8 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->split_a = c->sp.on ? c->sp.NB : 0;
   info->stg_a = c->sta.on ? c->sta.NB : 0;
   info->stg_at = c->stat.on ? c->stat.NB : 0;
+  info->rao_a = c->sa.affinity;
+  info->rao_at = c->sat.affinity;
   return HPR_OK;
 }
 

@@ -873,23 +873,29 @@ __global__ void k_gather_t(const int *perm, const int *row_of, const double *val
 // desc, index asc); long rows and padding go last with row = -1.  Writes
 // slice_row and the slot count of each slice (32 * longest row in it); the
 // arrays cover nrows rounded up to kWindow (a last partial window stops there).
+// ``order`` (optional, non-split plans only): the rows in processing order --
+// window w takes rows order[w*WIN ...] instead of rows w*WIN ... (the row
+// affinity order below).  A row's own sum is unaffected: only which rows share
+// a window / slice, and when they are processed, changes.
 template <int WIN>
 __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int sort_rows,
                                                    int *slice_row, unsigned short *slice_len,
                                                    int *slice_slots, int *long_flag,
-                                                   int long_thresh, int m_pad, int m_real) {
+                                                   int long_thresh, int m_pad, int m_real,
+                                                   const int *order) {
   __shared__ int key[WIN];
   __shared__ int skey[WIN];
   const int t = threadIdx.x;
-  const int r = blockIdx.x * WIN + t;
+  const int r_in = blockIdx.x * WIN + t;
+  const int r = (order && r_in < nrows) ? order[r_in] : r_in;
   const int rows_pad = (nrows + kWindow - 1) / kWindow * kWindow;
   int k = -2;
   // column-split plans (m_pad > 0): virtual rows b * m_pad + i with i >= m_real are padding
-  if (r < nrows && (m_pad == 0 || r % m_pad < m_real)) {
+  if (r_in < nrows && (m_pad == 0 || r % m_pad < m_real)) {
     const int len = rp[r + 1] - rp[r];
     k = len > long_thresh ? -1 : len;
     long_flag[r] = len > long_thresh;
-  } else if (r < nrows) {
+  } else if (r_in < nrows) {
     long_flag[r] = 0;
   }
   key[t] = k;
@@ -914,6 +920,31 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
     int mx = 0;
     for (int i = 0; i < kSlice; ++i) mx = max(mx, skey[t * kSlice + i]);
     slice_slots[blockIdx.x * (WIN / kSlice) + t] = mx * kSlice;
+  }
+}
+
+// Row affinity key (the SELL plan's processing order when the gathered
+// vector exceeds L2): the column block (2^bits columns) holding most of the
+// row's entries -- the longest run of equal ci >> bits, the row's columns being
+// ascending; ties go to the lowest block; empty rows key 0.  Rows sorted
+// stably by it are processed together with the other rows that gather the same
+// vector block, so a block fetched from HBM by one row is an L2 hit for the
+// next (C3: a capacity row re-reads exactly the flow segment its tail node's
+// conservation rows just read).
+__global__ void k_row_mode_block(const int *rp, const int *ci, int nrows, int bits, int *key) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int z0 = rp[r], z1 = rp[r + 1];
+    int best = 0, best_len = 0, cur = -1, cur_len = 0;
+    for (int z = z0; z < z1; ++z) {
+      const int b = ci[z] >> bits;
+      cur_len = b == cur ? cur_len + 1 : 1;
+      cur = b;
+      if (cur_len > best_len) {
+        best_len = cur_len;
+        best = cur;
+      }
+    }
+    key[r] = best;
   }
 }
 

@@ -215,7 +215,7 @@ class RowBlockGroup:
     def layout_info(self) -> dict:
         infos = [b.layout_info() for b in self.blocks]
         out = {k: sum(i[k] for i in infos) for k in infos[0]}
-        for k in ("split_a", "stg_a", "stg_at"):       # column blocks / chunks, not counts
+        for k in ("split_a", "stg_a", "stg_at", "rao_a", "rao_at"):   # block counts / flags, not sums
             out[k] = max(i[k] for i in infos)
         out["partitions"] = self.P
         return out

@@ -48,16 +48,54 @@ def _close(a, b, rel=TOL):
     return abs(a - b) <= rel * max(1.0, abs(b))
 
 
-def assert_report_parity(rep, g, name=""):
-    d = rep.to_json_dict(include_solution=False)
+def _rel_close(a, b, rel, floor=0.0):
+    """|a - b| <= rel * |b| + floor (both finite), or identical non-finite values."""
+    if not (np.isfinite(a) and np.isfinite(b)):
+        return (np.isnan(a) and np.isnan(b)) or a == b
+    return abs(a - b) <= rel * abs(b) + floor + 1e-300
+
+
+# sigma_next / merit / sigma_final: functions of device-reduced norms whose
+# only difference from the reference is the summation order of the dot
+# products (BLAS ddot vs a fixed-order tree) and the iterate rounding that
+# follows from it.  Both are norms of DIFFERENCES of iterates (x_bar - x0,
+# y_bar - y0: driver.py:264-278; w - w_bar: core.py:182-201), so they carry
+# the iterates' absolute agreement (~1e-15 on O(1) iterates), amplified by
+# |w| / |dw|.  The reference's own algorithm moves sigma_next by up to 4e-8
+# relative when ONLY its norms are summed in another order
+# (tests/test_oracle_golden.py::test_sigma_sensitivity_to_norm_order: exact
+# fsum norms, acceptance suite at 1e-8), so 1e-9 is unattainable by any
+# implementation; the bar is 5e-7 (the GPU measured <= 5e-8); the merit gets
+# an absolute floor of 1e-12 on top (it shrinks to ~1e-7).
+SIGMA_REL = 5e-7
+MERIT_FLOOR = 1e-12
+
+
+def assert_report_parity(rep, g, name="", tol=1e-8):
+    """Every field of the reference's report (driver.py:154-188) except the
+    timings: counts and triggers identical, objectives and all KKT fields
+    within 1e-8 * max(1, |ref|), restart sigma / merit and sigma_final within
+    SIGMA_REL relative (scaled up for solves deeper than 1e-8: the outer-loop
+    differences those norms measure shrink with the solve tolerance ``tol``,
+    the iterates' absolute agreement does not), lambda within 1e-12."""
+    srel = SIGMA_REL * max(1.0, 1e-8 / tol)
+    d = rep.to_json_dict(include_solution=False) if not isinstance(rep, dict) else rep
     assert d["status"] == g["status"], name
     assert d["iterations"] == g["iterations"], name
     assert d["restarts"] == g["restarts"], name
-    assert [e["trigger"] for e in d["restart_log"]] == [e["trigger"] for e in g["restart_log"]], name
-    assert [e["tau"] for e in d["restart_log"]] == [e["tau"] for e in g["restart_log"]], name
+    assert len(d["restart_log"]) == len(g["restart_log"]) == d["restarts"], name
+    for e, f in zip(d["restart_log"], g["restart_log"]):
+        assert (e["outer_index"], e["trigger"], e["tau"]) == (
+            f["outer_index"], f["trigger"], f["tau"]), (name, e, f)
+        assert _rel_close(e["sigma_next"], f["sigma_next"], srel), (name, "sigma_next", e, f)
+        assert _rel_close(e["merit"], f["merit"], srel, MERIT_FLOOR), (name, "merit", e, f)
+    assert _rel_close(d["sigma_final"], g["sigma_final"], srel), (
+        name, d["sigma_final"], g["sigma_final"])
     assert _close(d["primal_objective"], g["primal_objective"]), (name, d["primal_objective"])
     assert _close(d["dual_objective"], g["dual_objective"]), (name, d["dual_objective"])
-    for k in ("primal_infeas_rel", "dual_infeas_rel", "gap_rel"):
+    for k in ("primal_infeas_abs", "primal_infeas_rel", "dual_infeas_abs", "dual_infeas_rel",
+              "gap_abs", "gap_rel", "residual_vector_norm", "primal_objective",
+              "dual_objective"):
         assert _close(d["kkt"][k], g["kkt"][k]), (name, k, d["kkt"][k], g["kkt"][k])
     assert d["kkt"]["dual_clamped"] == g["kkt"]["dual_clamped"], name
     assert _close(d["lambda_estimate"], g["lambda_estimate"], 1e-12), name
@@ -69,13 +107,22 @@ def assert_report_parity(rep, g, name=""):
 
 # SELL-32-sigma / column-blocked smem-staged (HPR_CB) / SELL with A's columns
 # split into blocks whose running sums are carried block to block
-# (HPR_SPLIT_COLS) / staged segmented engine (HPR_STG, both phases)
-ENGINES = ["sell", "cb", "split", "stg"]
+# (HPR_SPLIT_COLS) / staged segmented engine (HPR_STG, both phases) / SELL
+# with both matrices' rows in the row-affinity order (HPR_RAO=1, 2^5-column
+# blocks so small problems get a non-trivial order)
+ENGINES = ["sell", "cb", "split", "stg", "rao"]
 
 
 def _engine_env(monkeypatch, engine, n):
     monkeypatch.setenv("HPR_CB", "1" if engine == "cb" else "0")
     monkeypatch.setenv("HPR_STG", "1" if engine == "stg" else "0")
+    if engine == "rao":
+        monkeypatch.setenv("HPR_RAO", "1")
+        monkeypatch.setenv("HPR_RAO_AT", "1")
+        monkeypatch.setenv("HPR_RAO_BITS", "5")
+    else:
+        monkeypatch.setenv("HPR_RAO", "0")
+        monkeypatch.setenv("HPR_RAO_AT", "0")
     if engine == "split":
         monkeypatch.setenv("HPR_SPLIT_COLS", str(max(1, -(-n // 7))))   # 7 column blocks
     else:
@@ -93,6 +140,7 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert (info["cb_a"] > 0 and info["cb_at"] > 0) == (engine == "cb")
     assert info["split_a"] == (7 if engine == "split" else 0)
     assert (info["stg_a"] > 0 and info["stg_at"] > 0) == (engine == "stg")
+    assert (info["rao_a"], info["rao_at"]) == ((1, 1) if engine == "rao" else (0, 0))
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.83, lam,
@@ -111,7 +159,7 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert np.array_equal(dev.to_host("x"), st.x)
 
 
-@pytest.mark.parametrize("engine", ["sell", "split", "stg"])
+@pytest.mark.parametrize("engine", ["sell", "split", "stg", "rao"])
 def test_iteration_bit_exact_midsize(engine, monkeypatch):
     """140k x 140k, 7 per row: >= 131072 rows (the HPR_SORT_WIN threshold) and
     the column-split A over seven 20k-column blocks."""
@@ -325,7 +373,7 @@ def test_small_cases_vs_reference(golden_reports):
         with warnings.catch_warnings(), np.errstate(all="ignore"):
             warnings.simplefilter("ignore")
             rep = P.solve(prob, P.SolverConfig(**case["cfg"]))
-        assert_report_parity(rep, case["report"], case["name"])
+        assert_report_parity(rep, case["report"], case["name"], case["cfg"]["tolerance"])
 
 
 def test_c1_vs_reference(golden_reports):
@@ -443,8 +491,4 @@ def test_flow_lp_downscaled_vs_oracle():
     cfg = dict(tolerance=1e-6, max_iterations=30000)
     rep = P.solve(prob, P.SolverConfig(**cfg))
     ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(**cfg))
-    assert rep.status.value == ref["status"]
-    assert rep.iterations == ref["iterations"]
-    assert [e.trigger for e in rep.restart_log] == [e["trigger"] for e in ref["restart_log"]]
-    assert _close(rep.primal_objective, ref["primal_objective"])
-    assert _close(rep.dual_objective, ref["dual_objective"])
+    assert_report_parity(rep, ref, "flow_lp_downscaled")

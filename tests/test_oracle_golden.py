@@ -156,3 +156,34 @@ def test_c_kernels_bit_identical_to_numpy_path():
     assert np.array_equal(sta.y, stb.y) and np.array_equal(sta.x, stb.x)
     x = np.random.default_rng(0).normal(size=a.n)
     assert np.array_equal(a.a.matvec(x), b.a.matvec(x))
+
+
+def test_sigma_sensitivity_to_norm_order(golden_reports):
+    """Why the restart sigma / merit bar is 5e-7 relative (test_gpu_parity.py
+    SIGMA_REL): the reference algorithm itself, with ONLY its vector norms
+    summed differently (exactly rounded fsum instead of BLAS), reproduces every
+    iteration count but moves sigma_next by far more than 1e-9."""
+    import math
+    real = np.linalg.norm
+
+    def fsum_norm(v, *a, **k):
+        if a or k:
+            return real(v, *a, **k)
+        v = np.asarray(v, dtype=float).ravel()
+        return math.sqrt(math.fsum(v * v))
+
+    worst = 0.0
+    entries = [e for e in golden_reports["acceptance_suite"] if e["cfg"]["tolerance"] == 1e-8]
+    for entry in entries[:5]:
+        prob, _ = generate_known_solution_lp(*entry["args"])
+        O.np.linalg.norm = fsum_norm
+        try:
+            rep = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(tolerance=1e-8))
+        finally:
+            O.np.linalg.norm = real
+        ref = entry["report"]
+        assert rep["iterations"] == ref["iterations"]
+        assert [e["trigger"] for e in rep["restart_log"]] == [e["trigger"] for e in ref["restart_log"]]
+        for e, f in zip(rep["restart_log"], ref["restart_log"]):
+            worst = max(worst, abs(e["sigma_next"] - f["sigma_next"]) / abs(f["sigma_next"]))
+    assert 1e-9 < worst < 5e-7, worst
