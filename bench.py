@@ -647,7 +647,7 @@ def run_ours(args):
             # (phases on the staged engine gather from shared memory instead)
             "roofline_gather": gather_roofline(nnz, its_total, iter_s_total, lay),
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": "rank-it/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": sample_clocks.summary(),

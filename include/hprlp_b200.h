@@ -210,6 +210,38 @@ int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
  * context's stream.  Requires hpr_analyze + hpr_bind_layout + hpr_scale. */
 int hpr_spmv(hpr_ctx *ctx, int transpose, const double *x, double *y);
 
+/* ------------------------------------------------------------------------
+ * Exact T1 = 0 path (csrc/hpr_exact.cuh).  Replaces
+ * the inner loop of solve_equality_exact (exact.py:125-129 ->
+ * hpr_exact_iterate, exact.py:83-91) and its checkpoint half step
+ * (exact_half_step, exact.py:70-80) for an equality-only problem (m1 == m)
+ * bound with identity scaling (hpr_scale(ctx, 0, 0, 0)).  The dense solve
+ * through the Cholesky factor L of AA* (solve_normal_equations,
+ * exact.py:62-67) is two triangular products with the explicit inverse
+ * factor: linv = L^{-1} (lower) and linv_t = L^{-T} (upper), both m x m
+ * row-major device arrays the caller computes once per solve.
+ * ------------------------------------------------------------------------ */
+typedef struct hpr_exact_bufs {
+  const double *linv;    /* m x m row-major, L^{-1} */
+  const double *linv_t;  /* m x m row-major, L^{-T} */
+  double *u;             /* n scratch: xb + sigma (zb - c) */
+  double *rhs;           /* m scratch: (b - A u) / sigma */
+  double *h;             /* m scratch: L^{-1} rhs */
+} hpr_exact_bufs;
+int hpr_exact_bind(hpr_ctx *ctx, const hpr_exact_bufs *bufs);
+/* `steps` exact iterations from counters (t, k) at penalty sigma (one CUDA
+ * graph replay per distinct `steps`); y, x advance in place; asynchronous. */
+int hpr_exact_run(hpr_ctx *ctx, int steps, int64_t t, int64_t k, double sigma, int variant);
+/* The half step at the current point: xb, zb -> xb/zb buffers and
+ * cand_x/cand_z[slot], yb -> yb and cand_y[slot]; then hpr_kkt(ctx, 1, slot)
+ * gives the residuals.  *nonfinite_k = first iteration with a non-finite
+ * iterate since hpr_state_reset, or -1.  Synchronises once. */
+int hpr_exact_half(hpr_ctx *ctx, double sigma, int slot, int64_t *nonfinite_k);
+/* y = L^{-T} (L^{-1} rhs) (solve_normal_equations, exact.py:62-67) with the
+ * inverse factors above; tmp: m scratch; asynchronous on `stream`. */
+int hpr_trsolve(int m, const double *linv, const double *linv_t, const double *rhs, double *tmp,
+                double *y, void *stream);
+
 /* Device time (ms) of the last hpr_run_inner and of the last checkpoint,
  * measured with CUDA events on the context stream. */
 int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);

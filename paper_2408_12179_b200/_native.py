@@ -113,6 +113,10 @@ class HprBatchResult(ctypes.Structure):
                                        "b_factor", "c_factor", "device_seconds")]
 
 
+class HprExactBufs(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("linv", "linv_t", "u", "rhs", "h")]
+
+
 # name -> (restype, argtypes); every int-returning function is error-checked
 _SIGS = {
     "hpr_abi_version": (ctypes.c_int, []),
@@ -147,6 +151,15 @@ _SIGS = {
     "hpr_spmv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "hpr_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
+    # exact T1 = 0 path (hpr_exact.cuh)
+    "hpr_exact_bind": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprExactBufs)]),
+    "hpr_exact_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_double, ctypes.c_int]),
+    "hpr_exact_half": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_int64)]),
+    "hpr_trsolve": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]),
     # row-block partitioned mode (hpr_rowblock.cuh)
     "hpr_nccl_available": (ctypes.c_int, []),
     "hpr_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),

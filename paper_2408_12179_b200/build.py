@@ -14,6 +14,7 @@ DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
               os.path.join(HERE, "csrc", "hpr_stg.cuh"),
               os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
               os.path.join(HERE, "csrc", "hpr_batch.cuh"),
+              os.path.join(HERE, "csrc", "hpr_exact.cuh"),
               os.path.join(ROOT, "include", "hprlp_b200.h")]
 OUT = os.path.join(HERE, "libhprlp_b200.so")
 

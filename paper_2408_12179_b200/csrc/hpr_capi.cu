@@ -21,6 +21,7 @@
 #include "hpr_kernels.cuh"
 #include "hpr_cb.cuh"
 #include "hpr_stg.cuh"
+#include "hpr_exact.cuh"
 
 using namespace hpr;
 
@@ -399,6 +400,20 @@ struct hpr_ctx {
   IterParams *h_params = nullptr;    // pinned
   PowState *h_pow = nullptr;         // pinned
   std::map<int, cudaGraphExec_t> inner_graphs;
+  // exact T1 = 0 path (hpr_exact.cuh): the inverse factor and scratch vectors,
+  // and its own per-interval graphs
+  struct Exact {
+    bool on = false;
+    const double *linv = nullptr, *linv_t = nullptr;
+    double *u = nullptr, *rhs = nullptr, *h = nullptr;
+    std::map<int, cudaGraphExec_t> graphs;
+  } exa;
+  void drop_inner_graphs() {
+    for (auto &kv : inner_graphs) cudaGraphExecDestroy(kv.second);
+    inner_graphs.clear();
+    for (auto &kv : exa.graphs) cudaGraphExecDestroy(kv.second);
+    exa.graphs.clear();
+  }
   cudaGraphExec_t pow_graph = nullptr;
   std::vector<long long> graph_sig;   // layout identity the graphs were captured against
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -1076,7 +1091,7 @@ int hpr_ctx_create(hpr_ctx **out, const hpr_dims *dims, int device, void *stream
 
 int hpr_ctx_destroy(hpr_ctx *c) {
   if (!c) return HPR_OK;
-  for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
+  c->drop_inner_graphs();
   if (c->pow_graph) cudaGraphExecDestroy(c->pow_graph);
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_params) cudaFreeHost(c->h_params);
@@ -1116,8 +1131,8 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
   c->params = (IterParams *)(c->ws + L.params);
   c->pow = (PowState *)(c->ws + L.pow);
   c->flags = (unsigned int *)(c->ws + L.flags);
-  for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
-  c->inner_graphs.clear();
+  c->drop_inner_graphs();
+  c->exa = hpr_ctx::Exact{};
   if (c->pow_graph) {
     cudaGraphExecDestroy(c->pow_graph);
     c->pow_graph = nullptr;
@@ -1238,8 +1253,7 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
                         (long long)C->seg_cap, (long long)C->stages, C->npad, C->nrpb})
       sig.push_back(v);
   if (sig != c->graph_sig) {
-    for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
-    c->inner_graphs.clear();
+    c->drop_inner_graphs();
     if (c->pow_graph) {
       cudaGraphExecDestroy(c->pow_graph);
       c->pow_graph = nullptr;
@@ -1374,8 +1388,7 @@ int hpr_scale(hpr_ctx *c, int ruiz_iters, int pock_chambolle, int bc_normalize,
   if (rc) return rc;
   const int bu = (hfl[0] ? 1 : 0) | (hfl[1] ? 2 : 0);
   if (bu != c->bounds_uniform || (bu && (std::memcmp(&hb[0], &c->lo_u, 8) || std::memcmp(&hb[1], &c->up_u, 8)))) {
-    for (auto &kv : c->inner_graphs) cudaGraphExecDestroy(kv.second);
-    c->inner_graphs.clear();
+    c->drop_inner_graphs();
   }
   c->bounds_uniform = bu;
   c->lo_u = hb[0];
@@ -1783,4 +1796,148 @@ extern "C" int hpr_spmv(hpr_ctx *c, int transpose, const double *x, double *y) {
   e.out = y;
   e.S = nullptr;
   return launch_sell(c, transpose ? c->mat_at(true) : c->mat_a(true), x, e, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// exact T1 = 0 path (hpr_exact.cuh; exact.py:62-91)
+// ---------------------------------------------------------------------------
+namespace {
+
+int launch_trmv_store(cudaStream_t s, const double *T, int m, int lower, const double *v,
+                      double *out) {
+  EpiTrStore e{out};
+  const int grid = (m + kTrThreads / 32 - 1) / (kTrThreads / 32);
+  k_trmv<EpiTrStore><<<grid, kTrThreads, 0, s>>>(T, m, lower, v, e);
+  CKL();
+  return HPR_OK;
+}
+
+// one exact iteration (half = 0) or the checkpoint's half step (half = 1)
+int exact_step(hpr_ctx *c, int step, int half, double sigma, int slot) {
+  const hpr_buffers &B = c->B;
+  const hpr_ctx::Exact &E = c->exa;
+  const int m = (int)c->d.m;
+  EpiExactX ex{};
+  ex.c = B.c_s;
+  ex.lo = B.lower_s;
+  ex.up = B.upper_s;
+  ex.anc = B.anc_x;
+  ex.x = B.x;
+  ex.u = E.u;
+  ex.xb_out = B.xb;
+  ex.zb_out = B.zb;
+  ex.cx_out = B.cand_x[slot];
+  ex.cz_out = B.cand_z[slot];
+  ex.P = c->params;
+  ex.step = step;
+  ex.half = half;
+  ex.sigma_half = sigma;
+  int rc = launch_sell(c, c->mat_at(true), B.y, ex, nullptr, nullptr);
+  if (rc) return rc;
+  EpiExactRhs er{};
+  er.b = B.b_s;
+  er.rhs = E.rhs;
+  er.P = c->params;
+  er.half = half;
+  er.sigma_half = sigma;
+  rc = launch_sell(c, c->mat_a(true), E.u, er, nullptr, nullptr);
+  if (rc) return rc;
+  rc = launch_trmv_store(c->stream, E.linv, m, 1, E.rhs, E.h);
+  if (rc) return rc;
+  EpiTrY ey{};
+  ey.anc = B.anc_y;
+  ey.y = B.y;
+  ey.yb_out = B.yb;
+  ey.cy_out = B.cand_y[slot];
+  ey.P = c->params;
+  ey.step = step;
+  ey.half = half;
+  const int grid = (m + kTrThreads / 32 - 1) / (kTrThreads / 32);
+  k_trmv<EpiTrY><<<grid, kTrThreads, 0, c->stream>>>(E.linv_t, m, 0, E.h, ey);
+  CKL();
+  c->launches += 2;
+  return HPR_OK;
+}
+
+}  // namespace
+
+extern "C" int hpr_exact_bind(hpr_ctx *c, const hpr_exact_bufs *eb) {
+  int rc = check_ctx(c, true, true);
+  if (rc) return rc;
+  if (!eb || !eb->linv || !eb->linv_t || !eb->u || !eb->rhs || !eb->h)
+    return fail(HPR_EINVAL, "null exact-path buffer");
+  if (c->d.m1 != c->d.m) return fail(HPR_EINVAL, "the exact path requires an equality-only instance");
+  for (auto &kv : c->exa.graphs) cudaGraphExecDestroy(kv.second);
+  c->exa.graphs.clear();
+  c->exa.linv = eb->linv;
+  c->exa.linv_t = eb->linv_t;
+  c->exa.u = eb->u;
+  c->exa.rhs = eb->rhs;
+  c->exa.h = eb->h;
+  c->exa.on = true;
+  return HPR_OK;
+}
+
+extern "C" int hpr_exact_run(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma,
+                             int variant) {
+  int rc = check_ctx(c, true, true);
+  if (rc) return rc;
+  if (!c->exa.on) return fail(HPR_ESTATE, "hpr_exact_bind first");
+  if (steps <= 0) return HPR_OK;
+  if (variant < 0 || variant > 2) return fail(HPR_EINVAL, "bad variant");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  auto it = c->exa.graphs.find(steps);
+  if (it == c->exa.graphs.end()) {
+    cudaGraph_t g;
+    const long long before = c->launches;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < steps; ++i) {
+      int rc2 = exact_step(c, i, 0, 0.0, 0);
+      if (rc2) {
+        cudaStreamEndCapture(s, &g);
+        return rc2;
+      }
+    }
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exe;
+    e = cudaGraphInstantiate(&exe, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(HPR_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    c->launches = before;   // captured, not executed
+    it = c->exa.graphs.emplace(steps, exe).first;
+  }
+  k_set_params<<<1, 1, 0, s>>>(c->params, sigma, 0.0, (long long)t, (long long)k, variant);
+  CKL();
+  CK(cudaEventRecord(c->ev0, s));
+  CK(cudaGraphLaunch(it->second, s));
+  CK(cudaEventRecord(c->ev1, s));
+  c->inner_timed = true;
+  c->launches += 1 + 4LL * steps;
+  return HPR_OK;
+}
+
+extern "C" int hpr_exact_half(hpr_ctx *c, double sigma, int slot, int64_t *nonfinite_k) {
+  int rc = check_ctx(c, true, true);
+  if (rc) return rc;
+  if (!c->exa.on) return fail(HPR_ESTATE, "hpr_exact_bind first");
+  if (slot < 0 || slot > 1 || !nonfinite_k) return fail(HPR_EINVAL, "bad argument");
+  CK(cudaSetDevice(c->device));
+  rc = exact_step(c, 0, 1, sigma, slot);
+  if (rc) return rc;
+  unsigned long long nf = 0;
+  CK(cudaMemcpyAsync(&nf, &c->params->nonfinite_k, sizeof(nf), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *nonfinite_k = nf == ULLONG_MAX ? -1 : (int64_t)nf;
+  return HPR_OK;
+}
+
+extern "C" int hpr_trsolve(int m, const double *linv, const double *linv_t, const double *rhs,
+                           double *tmp, double *y, void *stream) {
+  if (m <= 0 || !linv || !linv_t || !rhs || !tmp || !y) return fail(HPR_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = launch_trmv_store(s, linv, m, 1, rhs, tmp);
+  if (rc) return rc;
+  return launch_trmv_store(s, linv_t, m, 0, tmp, y);
 }

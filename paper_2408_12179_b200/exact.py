@@ -3,15 +3,23 @@
 For equality-only instances whose AA* is cheap to factor (m <= 2000), the
 reference (``/root/reference/pkg/src/hprlp/exact.py``) drops the proximal
 weight and solves the dual subproblem exactly through a dense Cholesky factor
-of AA*.  Here the factor lives in HBM (cuSOLVER ``potrf`` through
-``torch.linalg.cholesky_ex``; AA* from the CSR by cuSPARSE SpGEMM), the two
-triangular solves per iteration are cuBLAS ``trsv``-class calls, the sparse
-products are this library's SELL kernels (``hpr_spmv``: each row summed left
-to right from 0.0, like scipy's ``csr_matvec``) and the elementwise steps are
-fp64 device ops with every product and sum rounded separately.  The KKT
-residuals come from ``hpr_kkt`` on the original problem.  Nothing runs on the
-host but the scalar decisions (termination, restart, sigma) -- the same ones
-as ``driver.solve``.
+of AA*.  Here the iteration loop is this library's own kernels
+(``csrc/hpr_exact.cuh``), ``check_interval`` iterations per CUDA-graph replay
+with no host synchronisation inside the interval:
+
+* x side (A^T y, clip, zb, u = xb + sigma (zb - c), the variant step of x) and
+  the right-hand side (b - A u) / sigma: SELL kernels with fused epilogues,
+  every row summed left to right from 0.0 like scipy's ``csr_matvec``;
+* the two triangular solves of ``solve_normal_equations``: products with the
+  explicit inverse factor L^{-1} / L^{-T}, computed once per solve (setup:
+  cuSOLVER ``potrf`` via ``torch.linalg.cholesky_ex`` and one triangular solve
+  against the identity) -- fully parallel per iteration instead of m
+  dependent substitution steps; the y variant step and the non-finite probe
+  are fused into the second product.
+
+The checkpoint runs the same kernels in half-step mode, then ``hpr_kkt`` on
+the original problem; the host makes only the scalar decisions (termination,
+restart, sigma) -- the same ones as ``driver.solve``.
 
 Names, arguments, errors and report contents follow the reference:
 
@@ -21,12 +29,14 @@ Names, arguments, errors and report contents follow the reference:
 * ``sigma_update_exact``                                            exact.py:94-103
 * ``solve_equality_exact``                                          exact.py:106-178
 * ``hpr_no_prox_trace``, ``halpern_padmm_trace``, ``max_trace_gap``   exact.py:188-285
+  (diagnostic formulations for the trace tests: device tensor ops)
 
 Parity (tests/test_exact.py against fixtures made by the reference,
 tests/golden/make_exact_golden.py): identical status, iteration count and
 restart triggers, objectives and residual fields within 1e-8; traces of the
 two formulations within 1e-10 of each other and of the reference's.  Bitwise
-equality with LAPACK's Cholesky is not attainable (blocking order).
+equality with LAPACK's Cholesky substitution is not attainable (blocking
+order).
 """
 
 from __future__ import annotations
@@ -75,6 +85,8 @@ class DenseCholesky:
 
     factor: object   # torch.float64 tensor (m, m) on the GPU
     m: int
+    inverse: object = None     # L^{-1}, row-major (m, m)
+    inverse_t: object = None   # L^{-T}, row-major (m, m)
 
     @classmethod
     def from_matrix(cls, a, row_limit: int = CHOLESKY_ROW_LIMIT, device: int = 0
@@ -104,27 +116,43 @@ class DenseCholesky:
         scale = float(torch.linalg.norm(aat))
         if float(torch.linalg.norm(recon - aat)) > 1e-10 * max(scale, 1e-300):
             raise RankDeficiencyError("Cholesky reconstruction check failed")
-        return cls(factor=lower, m=m)
+        eye = torch.eye(m, dtype=torch.float64, device=dev)
+        inv = torch.linalg.solve_triangular(lower, eye, upper=False).contiguous()
+        return cls(factor=lower, m=m, inverse=inv, inverse_t=inv.T.contiguous())
 
 
 def solve_normal_equations(chol: DenseCholesky, rhs):
-    """Solve AA* y = rhs through the cached factor (exact.py:62-67); ``rhs`` a
-    device tensor (returned on the device) or a host array (returned on the
-    host)."""
+    """Solve AA* y = rhs through the cached factor (exact.py:62-67): the two
+    triangular solves as products with L^{-1} and L^{-T} (``hpr_trsolve``).
+    ``rhs`` a device tensor (returned on the device) or a host array
+    (returned on the host)."""
+    import ctypes
+    from . import _native as N
     torch = _torch()
     host = not isinstance(rhs, torch.Tensor)
-    r = torch.as_tensor(np.asarray(rhs, np.float64)).to(chol.factor.device) if host else rhs
+    dev = chol.factor.device
+    r = torch.as_tensor(np.asarray(rhs, np.float64)) if host else rhs
     if tuple(r.shape) != (chol.m,):
         raise ValueError("rhs length does not match the factor")
-    half = torch.linalg.solve_triangular(chol.factor, r.reshape(-1, 1), upper=False)
-    y = torch.linalg.solve_triangular(chol.factor.T, half, upper=True).reshape(-1)
-    return y.cpu().numpy() if host else y
+    r = r.to(device=dev, dtype=torch.float64).contiguous()
+    tmp = torch.empty(chol.m, dtype=torch.float64, device=dev)
+    y = torch.empty(chol.m, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    N.call("hpr_trsolve", int(chol.m), ctypes.c_void_p(chol.inverse.data_ptr()),
+           ctypes.c_void_p(chol.inverse_t.data_ptr()), ctypes.c_void_p(r.data_ptr()),
+           ctypes.c_void_p(tmp.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+           ctypes.c_void_p(stream.cuda_stream))
+    if host:
+        stream.synchronize()
+        return y.cpu().numpy()
+    return y
 
 
 class _Dev:
     """Device data of an equality-only problem: the SELL layout for the sparse
     products (identity scaling: the exact path is unpreconditioned), b, c,
-    bounds as device tensors, and the KKT evaluation on the original problem."""
+    bounds as device tensors, the KKT evaluation on the original problem, and
+    (``bind``) the exact-path kernels' inverse factors and scratch."""
 
     def __init__(self, problem, device: int):
         if int(problem.m2) != 0:
@@ -133,6 +161,7 @@ class _Dev:
         self.d = DeviceLP(problem, device=device)
         self.d.analyze()
         self.sc = self.d.scale(0, False, False)
+        self.d.state_reset()
         t = self.d.t
         self.m, self.n = self.d.m, self.d.n
         self.b, self.c = t["b_s"], t["c_s"][:self.n]
@@ -141,6 +170,48 @@ class _Dev:
         torch = _torch()
         self._ybuf = torch.empty(self.m + 8, dtype=torch.float64, device=self.d.device)
         self._xbuf = torch.empty(self.n + 8, dtype=torch.float64, device=self.d.device)
+        self._chol = None
+
+    def bind(self, chol: DenseCholesky):
+        """Hand the inverse factors and scratch vectors to hpr_exact_bind."""
+        import ctypes
+        from . import _native as N
+        if self._chol is chol:
+            return
+        torch = _torch()
+        f64 = dict(dtype=torch.float64, device=self.d.device)
+        with torch.cuda.stream(self.stream):
+            self._u = torch.empty(self.n + 8, **f64)
+            self._rhs = torch.empty(self.m + 8, **f64)
+            self._h = torch.empty(self.m + 8, **f64)
+        eb = N.HprExactBufs(chol.inverse.data_ptr(), chol.inverse_t.data_ptr(),
+                            self._u.data_ptr(), self._rhs.data_ptr(), self._h.data_ptr())
+        N.call("hpr_exact_bind", self.d.ctx, ctypes.byref(eb))
+        self._chol = chol
+
+    def run(self, steps, t, k, sigma, variant):
+        """``steps`` exact iterations on the device state (hpr_exact_run)."""
+        from . import _native as N
+        N.call("hpr_exact_run", self.d.ctx, int(steps), int(t), int(k), float(sigma),
+               N.VARIANT_CODE[getattr(variant, "value", variant)])
+
+    def half(self, sigma, slot=0) -> int:
+        """Half step at the device state into xb/zb/yb and candidate ``slot``;
+        returns the first non-finite iteration since the reset, or -1."""
+        import ctypes
+        from . import _native as N
+        nf = ctypes.c_int64(-1)
+        N.call("hpr_exact_half", self.d.ctx, float(sigma), int(slot), ctypes.byref(nf))
+        return int(nf.value)
+
+    def load(self, current, anchor=None):
+        """Device state <- (y, x) [and anchor] device tensors."""
+        t = self.d.t
+        t["y"][:self.m].copy_(current.y)
+        t["x"][:self.n].copy_(current.x)
+        if anchor is not None:
+            t["anc_y"][:self.m].copy_(anchor.y)
+            t["anc_x"][:self.n].copy_(anchor.x)
 
     def apply(self, x):
         """A x (sparse.py:102-104)."""
@@ -156,13 +227,15 @@ class _Dev:
         self.d.spmv(True, self._ybuf, out)
         return out
 
-    def kkt(self, y, x, z) -> KktResidual:
-        """driver.py:191-228 on the original problem (hpr_kkt)."""
+    def kkt(self, y=None, x=None, z=None, slot=0) -> KktResidual:
+        """driver.py:191-228 on the original problem (hpr_kkt) of candidate
+        ``slot`` (after storing (y, x, z) there when given)."""
         t = self.d.t
-        t["cand_y"][0][:self.m].copy_(y)
-        t["cand_x"][0][:self.n].copy_(x)
-        t["cand_z"][0][:self.n].copy_(z)
-        o = self.d.kkt(1, 0)
+        if y is not None:
+            t["cand_y"][slot][:self.m].copy_(y)
+            t["cand_x"][slot][:self.n].copy_(x)
+            t["cand_z"][slot][:self.n].copy_(z)
+        o = self.d.kkt(1, slot)
         return kkt_from_sums(o, self.sc.bnorm_orig, self.sc.cnorm_orig,
                              float(getattr(self.problem, "objective_constant", 0.0)))
 
@@ -193,53 +266,34 @@ class ExactState:
 
 
 def exact_half_step(state: ExactState, data: _Dev, chol: DenseCholesky):
-    """(xb, yb, zb) for the no-proximal dual update (exact.py:70-80)."""
-    y, x = state.current.y, state.current.x
-    sigma = state.sigma
-    v = x + sigma * (data.t_apply(y) - data.c)
-    xb = _clip(v, data.lower, data.upper)
-    zb = (xb - v) / sigma
-    rhs = (data.b - data.apply(xb + sigma * (zb - data.c))) / sigma
-    yb = solve_normal_equations(chol, rhs)
-    return xb, yb, zb
+    """(xb, yb, zb) for the no-proximal dual update (exact.py:70-80), by the
+    exact-path kernels in half-step mode on ``state.current``."""
+    data.bind(chol)
+    with _torch().cuda.stream(data.stream):
+        data.load(state.current)
+        data.half(state.sigma)
+        t = data.d.t
+        return t["xb"][:data.n].clone(), t["yb"][:data.m].clone(), t["zb"][:data.n].clone()
 
 
-def _clip(v, lo, up):
-    """np.clip(v, l, u) == minimum(maximum(v, l), u) with numpy's NaN rules."""
+def hpr_exact_iterate(state: ExactState, data: _Dev, chol: DenseCholesky):
+    """One iteration with the exact dual solve; same variant step as the lambda
+    path (exact.py:83-91): the half step, then one exact-path iteration on the
+    device (the same four kernels with the variant step fused)."""
     torch = _torch()
-    return torch.minimum(torch.maximum(v, lo), up)
-
-
-def _apply_variant_step(state: ExactState, yb, xb) -> None:
-    """core.py:139-160 (device tensors)."""
-    torch = _torch()
-    y, x = state.current.y, state.current.x
-    t2 = state.t + 2.0
-    w_new = (state.t + 1.0) / t2
-    w_anchor = 1.0 / t2
-    v = getattr(state.variant, "value", state.variant)
-    if v == "dr":
-        y_next, x_next = yb, xb
-    elif v == "hpr":
-        y_next = w_anchor * state.anchor.y + w_new * (2.0 * yb - y)
-        x_next = w_anchor * state.anchor.x + w_new * (2.0 * xb - x)
-    else:
-        y_next = w_anchor * state.anchor.y + w_new * yb
-        x_next = w_anchor * state.anchor.x + w_new * xb
+    if data is None or int(getattr(data, "problem").m2) != 0:
+        raise ValueError("the exact path requires an equality-only instance")
+    xb, yb, _ = exact_half_step(state, data, chol)
+    with torch.cuda.stream(data.stream):
+        data.load(state.current, state.anchor)
+        data.run(1, state.t, state.k, state.sigma, state.variant)
+        t = data.d.t
+        y_next, x_next = t["y"][:data.m].clone(), t["x"][:data.n].clone()
     if not bool(torch.isfinite(y_next).all() & torch.isfinite(x_next).all()):
         raise NumericalBreakdownError(state.k)
     state.current = ExactIterate(y_next, x_next)
     state.t += 1
     state.k += 1
-
-
-def hpr_exact_iterate(state: ExactState, data: _Dev, chol: DenseCholesky):
-    """One iteration with the exact dual solve; same variant step as the lambda
-    path (exact.py:83-91)."""
-    if data is None or int(getattr(data, "problem").m2) != 0:
-        raise ValueError("the exact path requires an equality-only instance")
-    xb, yb, _ = exact_half_step(state, data, chol)
-    _apply_variant_step(state, yb, xb)
     return xb, yb
 
 
@@ -277,7 +331,9 @@ def _merit_no_prox(dy, dx, sigma, data: _Dev) -> float:
 def solve_equality_exact(problem, cfg: SolverConfig | None = None, *, device: int = 0
                          ) -> SolveReport:
     """Restarted solve of an equality-only instance with exact dual solves
-    (exact.py:106-178), on the GPU.  No preconditioning is applied."""
+    (exact.py:106-178), on the GPU.  No preconditioning is applied.  Each
+    interval is one graph replay of the exact-path kernels; the checkpoint is
+    the half step + KKT (one synchronisation) and the host's scalar rules."""
     torch = _torch()
     cfg = SolverConfig.coerce(cfg) if cfg is not None else SolverConfig()
     if int(problem.m2) != 0:
@@ -288,27 +344,33 @@ def solve_equality_exact(problem, cfg: SolverConfig | None = None, *, device: in
     try:
         with torch.cuda.stream(data.stream):
             chol = DenseCholesky.from_matrix(problem.a_eq, device=device)
-            f64 = dict(dtype=torch.float64, device=data.d.device)
-            zero = ExactIterate(torch.zeros(data.m, **f64), torch.zeros(data.n, **f64))
-            state = ExactState(current=zero, anchor=ExactIterate(zero.y.clone(), zero.x.clone()),
-                               sigma=cfg.sigma0, variant=cfg.variant)
+            data.bind(chol)
+            t = data.d.t
+            m, n = data.m, data.n
+            cur_y, cur_x = t["y"][:m], t["x"][:n]          # the device state (origin)
+            anc_y, anc_x = t["anc_y"][:m], t["anc_x"][:n]
+            yb, xb, zb = t["yb"][:m], t["xb"][:n], t["zb"][:n]
+            state = ExactState(current=ExactIterate(cur_y, cur_x),
+                               anchor=ExactIterate(anc_y, anc_x), sigma=cfg.sigma0,
+                               variant=cfg.variant)
             restart_log: list[RestartEvent] = []
             status = None
             res = None
-            cand = None
             while status is None:
                 steps = min(cfg.check_interval, cfg.max_iterations - state.k)
                 t0 = time.perf_counter()
-                for _ in range(steps):
-                    hpr_exact_iterate(state, data, chol)
+                data.run(steps, state.t, state.k, state.sigma, state.variant)
                 data.stream.synchronize()
+                state.t += steps
+                state.k += steps
                 timings.iteration_seconds += time.perf_counter() - t0
 
                 t0 = time.perf_counter()
-                xb, yb, zb = exact_half_step(state, data, chol)
+                nonfinite = data.half(state.sigma, 0)
+                if nonfinite >= 0:
+                    raise NumericalBreakdownError(nonfinite)
                 state.bar = ExactIterate(yb, xb)
-                cand = (yb, zb, xb)
-                res = data.kkt(yb, xb, zb)
+                res = data.kkt(slot=0)
                 if check_termination(res, cfg.tolerance):
                     status = SolveStatus.OPTIMAL
                 elif state.k >= cfg.max_iterations:
@@ -316,8 +378,7 @@ def solve_equality_exact(problem, cfg: SolverConfig | None = None, *, device: in
                 elif time.perf_counter() - wall_start >= cfg.time_limit_seconds:
                     status = SolveStatus.TIME_LIMIT
                 elif cfg.variant.uses_restarts:
-                    merit_now = 2.0 * _merit_no_prox(state.current.y - yb, state.current.x - xb,
-                                                     state.sigma, data)
+                    merit_now = 2.0 * _merit_no_prox(cur_y - yb, cur_x - xb, state.sigma, data)
                     if state.merit_first is None:
                         state.merit_first = merit_now
                         state.merit_prev = math.inf
@@ -329,8 +390,7 @@ def solve_equality_exact(problem, cfg: SolverConfig | None = None, *, device: in
                         restart_log.append(RestartEvent(
                             outer_index=state.r, trigger=kind.value, tau=state.t,
                             sigma_next=sigma_next, merit=merit_now))
-                        state.anchor = ExactIterate(yb.clone(), xb.clone())
-                        state.current = ExactIterate(yb.clone(), xb.clone())
+                        data.d.restart()               # anchor = current = bar
                         state.sigma = sigma_next
                         state.r += 1
                         state.t = 0
@@ -338,7 +398,9 @@ def solve_equality_exact(problem, cfg: SolverConfig | None = None, *, device: in
                         state.merit_prev = math.inf
                 data.stream.synchronize()
                 timings.checkpoint_seconds += time.perf_counter() - t0
-            y, z, x = (v.cpu().numpy() for v in cand)
+            y = t["cand_y"][0][:m].cpu().numpy()
+            x = t["cand_x"][0][:n].cpu().numpy()
+            z = t["cand_z"][0][:n].cpu().numpy()
     finally:
         data.close()
     pobj, dobj = res.primal_objective, res.dual_objective
@@ -371,6 +433,12 @@ class AveragedTrace:
     y: list
     z: list
     x: list
+
+
+def _clip(v, lo, up):
+    """np.clip(v, l, u) == minimum(maximum(v, l), u) with numpy's NaN rules."""
+    torch = _torch()
+    return torch.minimum(torch.maximum(v, lo), up)
 
 
 def _z_step(data: _Dev, y, x, sigma):
