@@ -1,8 +1,10 @@
 """Batch of small LPs, one whole restarted HPR solve per CTA (config C5).
 
 ``solve_batch(problems, cfg)`` is ``[solve(p, cfg) for p in problems]``
-(reference ``driver.py:281-405`` per LP) executed as ONE kernel launch of
-``libhprlp_b200.so`` (``csrc/hpr_batch.cuh``): each CTA stages its LP in
+(reference ``driver.py:281-405`` per LP) executed as one kernel launch of
+``libhprlp_b200.so`` (``csrc/hpr_batch.cuh``) -- for large batches a pipeline
+of launches over chunks, overlapping host packing, upload, solve and report
+assembly (``_run_pipelined``) -- where each CTA stages its LP in
 shared memory and runs scaling, the power method, the inner loop, the
 checkpoints, restarts and sigma updates without returning to the host.
 ``solve_batch_sharded`` splits the batch across the ranks of a
@@ -14,6 +16,7 @@ from __future__ import annotations
 import ctypes
 import os
 import math
+import threading
 import warnings
 
 import numpy as np
@@ -202,7 +205,12 @@ class BatchRun:
     """Device residency of one packed batch + its native solve (re-runnable)."""
 
     def __init__(self, packed: PackedBatch, device: int = 0, stream=None, pinned: bool = True,
-                 max_log: int | None = None):
+                 max_log: int | None = None, staging=None):
+        """``staging``: the pinned uint8 tensor ``packed`` was packed into (the
+        pipelined ``solve_batch``): the upload is issued from it asynchronously
+        and ``self.h2d_done`` (an event) marks when the buffer may be reused;
+        otherwise the process-wide staging buffer is used and the upload is
+        waited for."""
         torch = _torch()
         self.max_log = int(MAX_LOG if max_log is None else max_log)
         if not torch.cuda.is_available():
@@ -223,8 +231,9 @@ class BatchRun:
             offs[k] = total
             total += (a.nbytes + 255) // 256 * 256
         self.t = {}
-        with _Staging.lock:
-            stage = _Staging.get(total)
+        self.h2d_done = None
+
+        def upload(stage):
             host = stage.numpy()
             base = host.ctypes.data
             for k, a in packed.arrays.items():
@@ -234,7 +243,15 @@ class BatchRun:
             with torch.cuda.stream(self.stream):
                 self._inputs = torch.empty(total, dtype=torch.uint8, device=self.device)
                 self._inputs.copy_(stage[:total], non_blocking=True)
-            self.stream.synchronize()
+
+        if staging is not None:
+            upload(staging)
+            self.h2d_done = torch.cuda.Event()
+            self.h2d_done.record(self.stream)
+        else:
+            with _Staging.lock:
+                upload(_Staging.get(total))
+                self.stream.synchronize()
         for k, a in packed.arrays.items():
             self.t[k] = self._inputs[offs[k]:offs[k] + a.nbytes].view(tdt[a.dtype])
         self.h2d_bytes = total
@@ -345,8 +362,91 @@ def _build_reports(pk: PackedBatch, raw, lraw, x, y, z, max_log: int = MAX_LOG) 
     return out
 
 
+PIPE_CHUNK = 1024      # LPs per pipelined launch (solve_batch on large batches)
+PIPE_MIN = 2048        # batches smaller than this run as one launch
+
+
+class _PipeStaging:
+    """Two process-wide pinned staging buffers per device (chunk j packs into
+    slot j % 2 while chunk j - 1's upload is in flight from the other);
+    ``lock`` serialises pipelined calls (they share the slots)."""
+
+    bufs: dict = {}
+    lock = threading.Lock()
+
+    @classmethod
+    def get(cls, device, slot, nbytes):
+        torch = _torch()
+        key = (device, slot)
+        b = cls.bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = cls.bufs[key] = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8,
+                                            pin_memory=True)
+        return b
+
+
+_PIPE_STREAMS = {}
+
+
+def _pipe_streams(torch, device):
+    st = _PIPE_STREAMS.get(device)
+    if st is None:
+        st = _PIPE_STREAMS[device] = [_batch_stream(torch, device),
+                                      torch.cuda.Stream(device=torch.device("cuda", device))]
+    return st
+
+
+def _launch_chunks(problems, cfg, device, streams, bounds):
+    """Pack, upload and launch every chunk; returns the BatchRuns."""
+    runs, pending = [], [None, None]
+    for j in range(len(bounds) - 1):
+        slot = j % 2
+        if pending[slot] is not None:
+            pending[slot].synchronize()           # that slot's previous upload is done
+        holder = {}
+
+        def stage(nb, slot=slot, holder=holder):
+            holder["t"] = _PipeStaging.get(device, slot, nb)
+            return holder["t"].numpy()
+
+        packed = PackedBatch(problems[bounds[j]:bounds[j + 1]], staging=stage)
+        run = BatchRun(packed, device=device, stream=streams[slot], staging=holder["t"])
+        packed.arrays = {}                        # views of the staging buffer: released
+        pending[slot] = run.h2d_done
+        run.launch(cfg)
+        runs.append(run)
+    for ev in pending:                            # the slots are free for the next call
+        if ev is not None:
+            ev.synchronize()
+    return runs
+
+
+def _run_pipelined(problems, cfg, device):
+    """Chunks of PIPE_CHUNK LPs: the host packs chunk j + 1 (into the other
+    pinned slot) while chunk j uploads and solves; consecutive chunks launch on
+    two streams so one launch's tail CTAs overlap the next launch's first
+    wave; chunk j's reports are built while the later chunks solve.  Every LP
+    is solved by its own CTA independently of the rest of the batch, so the
+    reports are identical to one launch over the whole batch."""
+    torch = _torch()
+    streams = _pipe_streams(torch, device)
+    bounds = list(range(0, len(problems), PIPE_CHUNK)) + [len(problems)]
+    with _PipeStaging.lock:
+        runs = _launch_chunks(problems, cfg, device, streams, bounds)
+    reps = []
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RestartLogOverflow)
+        for j, run in enumerate(runs):
+            for r in run.reports(cfg):
+                r.device_stats["batch_index"] += bounds[j]
+                reps.append(r)
+    return reps
+
+
 def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
-    """``[solve(p, cfg) for p in problems]`` as one device launch (one CTA per LP)."""
+    """``[solve(p, cfg) for p in problems]`` as device launches of one CTA per
+    LP (one launch, or pipelined chunks of PIPE_CHUNK LPs for batches of at
+    least PIPE_MIN)."""
     cfg = SolverConfig.coerce(cfg)
     if math.isfinite(cfg.time_limit_seconds):
         warnings.warn("batch time limits are measured per CTA on the device clock",
@@ -355,15 +455,18 @@ def solve_batch(problems, cfg=None, *, device: int = 0) -> list[SolveReport]:
     if not _torch().cuda.is_available():
         raise N.NativeUnavailableError("CUDA device required: the batch path has no CPU fallback")
     problems = list(problems)
-    with _Staging.lock:
-        # pack straight into the pinned staging buffer, then one H2D copy
-        packed = PackedBatch(problems, staging=lambda nb: _Staging.get(nb).numpy())
-        run = BatchRun(packed, device=device)
-        packed.arrays = {}                        # views of the staging buffer: released
-    run.launch(cfg)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore", RestartLogOverflow)
-        reps = run.reports(cfg)
+    if len(problems) >= PIPE_MIN and os.environ.get("HPR_BATCH_PIPE", "1") != "0":
+        reps = _run_pipelined(problems, cfg, device)
+    else:
+        with _Staging.lock:
+            # pack straight into the pinned staging buffer, then one H2D copy
+            packed = PackedBatch(problems, staging=lambda nb: _Staging.get(nb).numpy())
+            run = BatchRun(packed, device=device)
+            packed.arrays = {}                    # views of the staging buffer: released
+        run.launch(cfg)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RestartLogOverflow)
+            reps = run.reports(cfg)
     over = [i for i, r in enumerate(reps) if r.restarts > len(r.restart_log)]
     if over:
         # the reference logs every restart: re-solve the LPs whose log overflowed

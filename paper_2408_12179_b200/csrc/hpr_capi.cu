@@ -1131,6 +1131,11 @@ int hpr_bind(hpr_ctx *c, const hpr_buffers *bufs, void *workspace, size_t ws_byt
   c->params = (IterParams *)(c->ws + L.params);
   c->pow = (PowState *)(c->ws + L.pow);
   c->flags = (unsigned int *)(c->ws + L.flags);
+  // the whole result / parameter blocks are read back at every checkpoint:
+  // defined contents even in the slots a given call does not write
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(c->results, 0, sizeof(double) * R_COUNT, c->stream));
+  CK(cudaMemsetAsync(c->params, 0, sizeof(IterParams), c->stream));
   c->drop_inner_graphs();
   c->exa = hpr_ctx::Exact{};
   if (c->pow_graph) {

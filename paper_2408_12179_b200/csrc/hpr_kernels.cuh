@@ -207,6 +207,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   } while (!ok);
 }
 
+#ifndef HPR_GA_LEAN
+#define HPR_GA_LEAN 0   // 1: gather-ahead pipeline loads values one batch ahead (fewer registers)
+#endif
+
 // ---------------------------------------------------------------------------
 // the SELL engine
 // ---------------------------------------------------------------------------
@@ -269,7 +273,41 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       c[u] = ld_stream(cp + u * kSlice, pol);
       v[u] = ld_stream(vp + u * kSlice, pol);
     }
-  if constexpr (GA) {
+  if constexpr (GA && HPR_GA_LEAN) {
+  // lean depth-2 pipeline: batch k+1's gathers and batch k+2's column
+  // indices are in flight while batch k's products are added; batch k+1's
+  // values are loaded one batch (not two) ahead -- 8 fewer live registers
+  double x0[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < len) x0[u] = ld_gather(xg + c[u]);
+  int c1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (U + u < len) c1[u] = ld_stream(cp + (U + u) * kSlice, pol);
+  for (int k = 0; k < slen; k += U) {
+    double x1[U], v1[U];
+    int c2[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + U + u < len) {
+        x1[u] = ld_gather(xg + c1[u]);
+        v1[u] = ld_stream(vp + (k + U + u) * kSlice, pol);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + 2 * U + u < len) c2[u] = ld_stream(cp + (k + 2 * U + u) * kSlice, pol);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], x0[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = v1[u];
+      x0[u] = x1[u];
+      c1[u] = c2[u];
+    }
+  }
+  } else if constexpr (GA) {
   // depth-2 pipeline: batch k+1's operand gathers and batch k+2's matrix loads
   // are in flight while batch k's products are added (long rows: the gather
   // latency is exposed once per two batches instead of once per batch)
@@ -410,8 +448,11 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
 #ifndef HPR_SELL_MINB
 #define HPR_SELL_MINB 6      // min resident CTAs per SM (register cap 80: C3 1033 -> 946 us/iteration)
 #endif
+#ifndef HPR_SELL_MINB_GA
+#define HPR_SELL_MINB_GA HPR_SELL_MINB   // the gather-ahead (long-row) instances
+#endif
 template <int U, bool GA, class Epi>
-__global__ void __launch_bounds__(kThreads, HPR_SELL_MINB)
+__global__ void __launch_bounds__(kThreads, GA ? HPR_SELL_MINB_GA : HPR_SELL_MINB)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll
@@ -1164,6 +1205,7 @@ __global__ void k_reset_params(IterParams *P) {
   P->t0 = 0;
   P->k0 = 0;
   P->variant = 0;
+  P->pad_ = 0;
   P->nonfinite_k = ~0ULL;
 }
 

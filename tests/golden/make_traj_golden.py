@@ -12,8 +12,10 @@ Writes:
   iterates (``hprlp``: ``scale_problem`` -> ``ProblemData.from_problem`` ->
   ``power_method_lambda_max`` -> ``iterate_once`` x 100, i.e. the preamble of
   ``driver.solve``, driver.py:293-309, and core.py:163-174): per-iteration
-  norms of y and x, the entries of y and x at 4096 fixed sampled indices at
-  the snapshot iterations, lambda and the power-iteration count; C2 also the
+  norms of y and x, the entries of y and x at ~4096 sampled indices (half
+  from the support of the k = 100 iterate) at the snapshot iterations, the
+  checksums y.r_m and x.r_n at the snapshots (r: fixed uniform(-1, 1) probe
+  vectors from ``probe_seed``), lambda and the power-iteration count; C2 also the
   full (y, x) at k = 100.  The instance is this package's generator output,
   pinned by the sha256 of every array (``inst_sha``).
 * ``c3_oracle_report.json`` -- the oracle's full C3 solve to 1e-8 (the
@@ -91,21 +93,33 @@ def reference_trajectory(name, full_snapshot):
           flush=True)
     st = SolverState.origin(data, sigma=1.0, lam=est.value)
     rng = np.random.default_rng(12345)
-    iy = np.sort(rng.choice(data.m, size=min(NSAMPLE, data.m), replace=False))
-    ix = np.sort(rng.choice(data.n, size=min(NSAMPLE, data.n), replace=False))
-    norms, sy, sx = [], [], []
+    # fixed probe vectors: per-snapshot checksums y.r_m, x.r_n over the whole iterate
+    rm, rn = rng.uniform(-1.0, 1.0, data.m), rng.uniform(-1.0, 1.0, data.n)
+    norms, snaps, dots = [], {}, []
     for k in range(1, 101):
         iterate_once(st, data)
         y, x = st.current.y, st.current.x
         norms.append((float(np.linalg.norm(y)), float(np.linalg.norm(x))))
         if k in SNAP_K:
-            sy.append(y[iy].copy())
-            sx.append(x[ix].copy())
+            snaps[k] = (y.copy(), x.copy())
+            dots.append((float(y @ rm), float(x @ rn)))
     print(f"{name}: 100 iterations at {time.time() - t0:.1f}s", flush=True)
+
+    def pick(v, size):
+        # half the sample from the support at k = 100 (sparse iterates), half uniform
+        nz = np.flatnonzero(v)
+        a = rng.choice(nz, size=min(size // 2, nz.size), replace=False) if nz.size else nz
+        b = rng.choice(v.size, size=min(size - a.size, v.size), replace=False)
+        return np.unique(np.concatenate([a, b]))
+
+    iy, ix = pick(snaps[100][0], NSAMPLE), pick(snaps[100][1], NSAMPLE)
+    sy = [snaps[k][0][iy] for k in SNAP_K]
+    sx = [snaps[k][1][ix] for k in SNAP_K]
     out = dict(inst_sha=np.array(digest), lam=np.array([est.value, est.raw]),
                power_iterations=np.array(est.iterations), snap_k=np.array(SNAP_K),
                idx_y=iy, idx_x=ix, snap_y=np.array(sy), snap_x=np.array(sx),
-               norms=np.array(norms), b_factor=np.array(info.b_norm_factor),
+               norms=np.array(norms), dots=np.array(dots), probe_seed=np.array(12345),
+               b_factor=np.array(info.b_norm_factor),
                c_factor=np.array(info.c_norm_factor))
     if full_snapshot:
         out["y100"] = st.current.y.copy()

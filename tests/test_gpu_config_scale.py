@@ -63,6 +63,11 @@ def _trajectory_check(name, prob, d, full=False):
     done = 0
     iy = torch.from_numpy(d["idx_y"]).to(dev.device)
     ix = torch.from_numpy(d["idx_x"]).to(dev.device)
+    probes = None
+    if "dots" in d.files:
+        rng = np.random.default_rng(int(d["probe_seed"]))
+        probes = (torch.from_numpy(rng.uniform(-1.0, 1.0, prob.m)).to(dev.device),
+                  torch.from_numpy(rng.uniform(-1.0, 1.0, prob.n)).to(dev.device))
     for i, k in enumerate(d["snap_k"]):
         dev.run_inner(int(k) - done, done, done, 1.0, lam, 2)
         done = int(k)
@@ -70,6 +75,12 @@ def _trajectory_check(name, prob, d, full=False):
         y, x = dev.t["y"], dev.t["x"][:prob.n]
         ny, nx = d["norms"][k - 1]
         assert abs(_norm(y) - ny) <= 1e-10 * ny and abs(_norm(x) - nx) <= 1e-10 * nx, (name, k)
+        if probes is not None:
+            # whole-iterate checksums y.r_m, x.r_n (summation order differs from
+            # numpy's: bounded by 1e-10 |v| |r|)
+            for v, r, ref in ((y, probes[0], d["dots"][i][0]), (x, probes[1], d["dots"][i][1])):
+                got = float(torch.dot(v, r).item())
+                assert abs(got - ref) <= 1e-10 * _norm(v) * _norm(r), (name, k, got, ref)
         gy, gx = y[iy].cpu().numpy(), x[ix].cpu().numpy()
         ry, rx = d["snap_y"][i], d["snap_x"][i]
         num = np.sqrt(np.sum((gy - ry) ** 2) + np.sum((gx - rx) ** 2))
