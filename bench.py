@@ -614,6 +614,8 @@ def run_ours(args):
     if rank == 0:
         r0 = reps[-1]
         lay = r0.device_stats.get("layout", {})
+        bu = int(lay.get("bounds_uniform", 0))
+        b_req = bi - 8 * n * ((bu & 1) + ((bu >> 1) & 1))
         cpu = cpu_baseline_sample(prob) if ws == 1 and not args.no_cpu else None
         if cpu is not None:
             cpu["host"] = host_info()
@@ -640,6 +642,9 @@ def run_ours(args):
                          else load_traffic(config),
                          "kernel": iteration_kernels(lay),
                          "bytes_per_iteration": bi, "peak_source": peak_kind,
+                         # l / u passed as scalars when uniform: bytes the pair must move
+                         "bytes_required": b_req,
+                         "frac_required": b_req * its_total / iter_s_total / 1e9 / peak,
                          "timing": "CUDA events on the solver stream around each "
                                    "150-iteration graph replay (the two iteration kernels)"},
             # the bound that actually binds a small-n problem (C2): every nonzero
@@ -866,27 +871,21 @@ def run_c4(args, dist, ws, rank, local):
     # uploads the block (pinned staging -> H2D), builds the rank group and runs
     # solve() for two 150-iteration intervals (analyse, scale, power method,
     # checkpoints, finalize, solution D2H); graphs are captured anew each time
-    import types
-    shell = types.SimpleNamespace(objective_constant=0.0, objective_negated=False)
+    from paper_2408_12179_b200.rowblock import solve_row_block
     cfg = P.SolverConfig(tolerance=1e-8, max_iterations=2 * interval, check_interval=interval)
-    e2e_t, e2e_its, h2d = 0.0, 0, 0
+    e2e_t, e2e_its = 0.0, 0
+    h2d = 0
     for _ in range(max(1, min(args.steps, 2))):
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
-        nid = broadcast_nccl_id(rank) if dist is not None else nccl_unique_id()
-        g2 = RowBlockGroup.distributed(block, n=C4_N, m_total=m, m1_total=m1,
-                                       nnz_total=m * C4_PER_ROW, row0=r0, rank=rank, world=ws,
-                                       nccl_id=nid, device=local)
-        try:
-            rep = P.solve(shell, cfg, dev=g2)
-            torch.cuda.synchronize()
-            e2e_t += time.perf_counter() - t0
-            e2e_its += rep.iterations
-            h2d = g2.h2d_bytes
-        finally:
-            g2.close()
+        rep = solve_row_block(block, cfg, n=C4_N, m_total=m, m1_total=m1,
+                              nnz_total=m * C4_PER_ROW, row0=r0, device=local)
+        torch.cuda.synchronize()
+        e2e_t += time.perf_counter() - t0
+        e2e_its += rep.iterations
+        h2d = rep.device_stats["h2d_bytes"]
     t_e2e, _ = _max_sum(dist, local, e2e_t, 0)
     e2e_val = ws * e2e_its / t_e2e
     peak, peak_kind = load_peaks()

@@ -199,6 +199,8 @@ typedef struct hpr_layout_info_t {
   int64_t split_a;       /* column blocks of A's split y-phase layout (0: not split) */
   int64_t stg_a, stg_at; /* staged-engine vector chunks of A / A^T (0: engine off) */
   int64_t rao_a, rao_at; /* 1: SELL rows in the row-affinity order (gathered vector > L2) */
+  int64_t bounds_uniform; /* after hpr_scale: bit 0 every scaled lower bound equal, bit 1
+                             every upper bound equal (passed as scalars, not streamed) */
 } hpr_layout_info_t;
 int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 

@@ -11,7 +11,7 @@ from .driver import (KktResidual, RestartEvent, RestartKind, SolveReport, Solver
                      SolveStatus, Timings, Variant, check_restart, check_termination,
                      kkt_residual, sigma_guards_pass, solve)
 from .batch import solve_batch, solve_batch_sharded
-from .rowblock import solve_distributed
+from .rowblock import solve_distributed, solve_row_block
 from .generators import generate_flow_lp, generate_known_solution_lp, generate_planted_lp_fast
 from .exact import (halpern_padmm_trace, hpr_no_prox_trace, max_trace_gap, solve_equality_exact,
                     solve_normal_equations)
@@ -30,5 +30,5 @@ __all__ = [
     "generate_flow_lp", "halpern_padmm_trace", "hpr_no_prox_trace", "max_trace_gap",
     "solve_equality_exact", "solve_normal_equations", "generate_known_solution_lp", "generate_planted_lp_fast",
     "kkt_residual", "primal_objective", "project_onto_box", "project_onto_dual_cone",
-    "sigma_guards_pass", "solve", "solve_batch", "solve_batch_sharded", "solve_distributed",
+    "sigma_guards_pass", "solve", "solve_batch", "solve_batch_sharded", "solve_distributed", "solve_row_block",
 ]

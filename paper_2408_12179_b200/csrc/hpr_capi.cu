@@ -63,6 +63,12 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
+#ifndef HPR_X_IMPLICIT
+#define HPR_X_IMPLICIT 1    // HPR inner loop: x re-formed from w inside an interval (EpiXIter)
+#endif
+#ifndef HPR_COMPACT_HDR
+#define HPR_COMPACT_HDR 1   // compact SELL slices (32 consecutive equal-length rows) skip the per-lane header
+#endif
 #ifndef HPR_POW_BATCH
 #define HPR_POW_BATCH 16   // 8 / 16 / 32 measured 17.55-17.73 / 17.78-17.79 / 17.76-17.78 k it/s on C2
 #endif
@@ -102,7 +108,7 @@ int64_t windows_of(int64_t nrows) { return (nrows + kWindow - 1) / kWindow; }
 
 // per-matrix plan arrays in the main workspace
 struct PlanOff {
-  size_t slice_row, slice_len, slice_slots, slice_ptr, long_flag, long_rows, nsel;
+  size_t slice_row, slice_len, slice_slots, slice_ptr, slice_base, long_flag, long_rows, nsel;
 };
 
 // column-blocked (CB) engine plan arrays of one matrix (persistent, workspace)
@@ -256,6 +262,7 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
     p.slice_len = take(sizeof(unsigned short) * nw * kWindow);
     p.slice_slots = take(sizeof(int) * (ns + 1));
     p.slice_ptr = take(sizeof(int) * (ns + 1));
+    p.slice_base = take(sizeof(int) * ns);
     p.long_flag = take(sizeof(int) * nrows);
     p.long_rows = take(sizeof(int) * nrows);
     p.nsel = take(sizeof(int));
@@ -341,7 +348,8 @@ struct Sell {
   int nrows = 0, nslices = 0, nlong = 0;
   long long slots = 0;
   unsigned short *slice_len = nullptr;
-  int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *long_flag = nullptr,
+  int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *slice_base = nullptr,
+      *long_flag = nullptr,
       *long_rows = nullptr, *nsel = nullptr;
   int *ci = nullptr, *pos = nullptr;
   double *val_s = nullptr, *val0 = nullptr;
@@ -423,7 +431,7 @@ struct hpr_ctx {
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
     const int ga = S.nslices > 0 && S.slots >= (long long)HPR_GA_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
-                   S.long_rows, S.nslices, S.nlong, ga, 0};
+                   S.long_rows, S.nslices, S.nlong, ga, 0, HPR_COMPACT_HDR ? S.slice_base : nullptr};
   }
   CbMat cbmat(const Cb &C, int ncols) const {
     return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
@@ -604,6 +612,7 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   S.slice_len = (unsigned short *)(c->ws + po.slice_len);
   S.slice_slots = (int *)(c->ws + po.slice_slots);
   S.slice_ptr = (int *)(c->ws + po.slice_ptr);
+  S.slice_base = (int *)(c->ws + po.slice_base);
   S.long_flag = (int *)(c->ws + po.long_flag);
   S.long_rows = (int *)(c->ws + po.long_rows);
   S.nsel = (int *)(c->ws + po.nsel);
@@ -612,11 +621,11 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   if (win == kSortWinBig)
     k_sell_plan<kSortWinBig><<<(nrows + win - 1) / win, win, 0, s>>>(
         rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots, S.long_flag, long_thresh, m_pad,
-        m_real, order);
+        m_real, order, S.slice_base);
   else
     k_sell_plan<kWindow><<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len,
                                                 S.slice_slots, S.long_flag, long_thresh, m_pad,
-                                                m_real, order);
+                                                m_real, order, S.slice_base);
   S.affinity = order != nullptr;
   CKL();
   size_t tb = c->L.cub_bytes;
@@ -1599,6 +1608,9 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     for (int i = 0; i < steps; ++i) {
       ex.step = i;
       ey.step = i;
+      // HPR: x implicit between the interval's first read and last write
+      ex.x_from_w = HPR_X_IMPLICIT && i > 0;
+      ex.x_store = !HPR_X_IMPLICIT || i == steps - 1;
       // the first kernel of the graph follows the k_set_params launch: plain edge
       int rc2 = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
                 : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
@@ -1774,6 +1786,7 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->stg_at = c->stat.on ? c->stat.NB : 0;
   info->rao_a = c->sa.affinity;
   info->rao_at = c->sat.affinity;
+  info->bounds_uniform = c->bounds_uniform;
   return HPR_OK;
 }
 

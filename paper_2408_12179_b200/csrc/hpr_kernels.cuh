@@ -124,6 +124,10 @@ struct SellMat {
   int nlong;
   int ga;                  // long rows: gather one batch ahead (HPR_GA_MIN)
   int keep;                // L2 policy of the matrix streams: 0 evict_first, 1 evict_last, 2 normal
+  // nslices (or nullptr): b >= 0 marks a compact slice -- lane i owns row b + i
+  // and every row has the slice's length -- whose per-lane header
+  // (slice_row / slice_len, 6 bytes a row) is then never read; -1 otherwise
+  const int *slice_base;
 };
 
 constexpr int kSlice = 32;
@@ -208,7 +212,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 #ifndef HPR_GA_LEAN
-#define HPR_GA_LEAN 0   // 1: gather-ahead pipeline loads values one batch ahead (fewer registers)
+#define HPR_GA_LEAN 1   // gather-ahead pipeline loads values one batch ahead: 8 fewer live registers (C2 -1.1 %)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -226,10 +230,16 @@ struct SliceHdr {
 __device__ __forceinline__ SliceHdr load_hdr(const SellMat &M, int s, int lane) {
   SliceHdr h{-1, 0, 0, 0};
   if (s < M.nslices) {
-    h.row = M.slice_row[s * kSlice + lane];
-    h.len = M.slice_len[s * kSlice + lane];
     h.base = M.slice_ptr[s];
     h.slen = (M.slice_ptr[s + 1] - h.base) / kSlice;
+    const int b = M.slice_base ? M.slice_base[s] : -1;
+    if (b >= 0) {
+      h.row = b + lane;
+      h.len = h.slen;
+    } else {
+      h.row = M.slice_row[s * kSlice + lane];
+      h.len = M.slice_len[s * kSlice + lane];
+    }
   }
   return h;
 }
@@ -499,6 +509,15 @@ k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
 // ---------------------------------------------------------------------------
 // x phase over A^T rows (core.py:168-169 + 149-153): x updated in place,
 // w = 2 xb - x for the y phase.
+//
+// HPR (variant 2) keeps x implicit inside an interval: x_{k+1} = wa_k anc +
+// wn_k w_k exactly (core.py:149-150), so a step with x_from_w set re-forms
+// x_k from the previous step's w (same operands, same rounding: the same
+// bits) instead of reading x, and a step without x_store skips the x write
+// -- one n-vector of HBM traffic less per iteration.  The inner-loop graph
+// sets x_from_w on steps 1.. and x_store on the last step only, so x is
+// materialised at every interval end (checkpoint, restart, the host); other
+// variants always read and write x.
 struct EpiXIter {
   static constexpr int NQ = 0;
   const double *c, *lo, *up, *anc;
@@ -506,30 +525,34 @@ struct EpiXIter {
   IterParams *P;
   int step;
   int bounds_uniform;        // bit 0: every lower bound equals lo_u, bit 1: upper / up_u
+  int x_from_w = 0, x_store = 1;
   double lo_u, up_u;
-  double sigma, wa, wn, xj, cj, lj, uj, aj;
-  int variant;
+  double sigma, wa, wn, wa0, wn0, xj, cj, lj, uj, aj;
+  int variant, implicit;
   __device__ bool enter() {
     sigma = P->sigma;
     variant = P->variant;
     halpern_weights(P->t0 + step, wa, wn);
+    implicit = variant == 2 && x_from_w;
+    if (implicit) halpern_weights(P->t0 + step - 1, wa0, wn0);
     return true;
   }
   __device__ void prefetch(int j) {
-    xj = ld_epi(x + j);
+    xj = ld_epi(implicit ? w + j : x + j);
     cj = ld_epi(c + j);
     lj = (bounds_uniform & 1) ? lo_u : ld_epi(lo + j);
     uj = (bounds_uniform & 2) ? up_u : ld_epi(up + j);
     aj = variant ? ld_epi(anc + j) : 0.0;
   }
   __device__ void finish(int j, double aty, double *) {
+    if (implicit) xj = __dadd_rn(__dmul_rn(wa0, aj), __dmul_rn(wn0, xj));   // x_k from w_{k-1}
     const double v = __dadd_rn(xj, __dmul_rn(sigma, __dsub_rn(aty, cj)));
     const double xb = np_clip(v, lj, uj);
     const double wj = __dsub_rn(__dmul_rn(2.0, xb), xj);
     const double xn =
         variant == 0 ? xb : __dadd_rn(__dmul_rn(wa, aj), __dmul_rn(wn, variant == 2 ? wj : xb));
     w[j] = wj;
-    x[j] = xn;
+    if (x_store || variant != 2) x[j] = xn;
     if (!isfinite(xn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
   }
 };
@@ -923,9 +946,10 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
                                                    int *slice_row, unsigned short *slice_len,
                                                    int *slice_slots, int *long_flag,
                                                    int long_thresh, int m_pad, int m_real,
-                                                   const int *order) {
+                                                   const int *order, int *slice_base) {
   __shared__ int key[WIN];
   __shared__ int skey[WIN];
+  __shared__ int srow[WIN];
   const int t = threadIdx.x;
   const int r_in = blockIdx.x * WIN + t;
   const int r = (order && r_in < nrows) ? order[r_in] : r_in;
@@ -950,6 +974,7 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
     }
   }
   skey[rank] = k;
+  srow[rank] = k >= 0 && m_pad == 0 ? r : -1;
   const int p = blockIdx.x * WIN + rank;
   if (p < rows_pad) {
     // column-split plans store the real row i of virtual row b * m_pad + i
@@ -961,6 +986,13 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
     int mx = 0;
     for (int i = 0; i < kSlice; ++i) mx = max(mx, skey[t * kSlice + i]);
     slice_slots[blockIdx.x * (WIN / kSlice) + t] = mx * kSlice;
+    // compact slice: 32 consecutive rows of equal length (no per-lane header)
+    const int r0 = srow[t * kSlice];
+    bool compact = r0 >= 0;
+    for (int i = 1; i < kSlice && compact; ++i)
+      compact = srow[t * kSlice + i] == r0 + i && skey[t * kSlice + i] == mx;
+    compact = compact && skey[t * kSlice] == mx;
+    slice_base[blockIdx.x * (WIN / kSlice) + t] = compact ? r0 : -1;
   }
 }
 

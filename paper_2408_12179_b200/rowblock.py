@@ -267,40 +267,67 @@ class RowBlockGroup:
         cols = (np.arange(k)[:, None] * (self.P * cw) + g * cw + np.arange(cw)[None, :]).ravel()
         return cols[cols < self.n]
 
+    def _gather_dev(self):
+        """(torch.distributed module, tensor device) for the host-side gathers:
+        the GPU over NCCL when the default group is NCCL, else host tensors
+        (gloo)."""
+        import torch.distributed as dist
+        if dist.get_backend() == "nccl":
+            return dist, self.blocks[0].device
+        return dist, "cpu"
+
     def to_host(self, name, slot=None):
-        """Row vectors: the ranks' blocks concatenated (all-gathered over
-        torch.distributed in NCCL mode).  Column vectors: assembled from each
-        rank's own slice (the only part a rank keeps current)."""
+        """Row vectors: the ranks' blocks concatenated.  Column vectors:
+        assembled from each rank's own slice (the only part a rank keeps
+        current).  In NCCL mode the pieces move with tensor all-gathers over
+        the job's torch.distributed group (device buffers over NVLink with the
+        NCCL backend), not through pickled host objects."""
+        torch = _torch()
         row_names = ("y", "anc_y", "yb", "dy", "b_s", "row_scale", "cand_y", "b")
         if name in row_names:
-            parts = [b.to_host(name, slot) for b in self.blocks]
-            if self.nccl and self.P > 1:
-                import torch.distributed as dist
-                got = [None] * self.P
-                dist.all_gather_object(got, parts[0])
-                parts = got
-            return np.concatenate(parts)
+            if not (self.nccl and self.P > 1):
+                return np.concatenate([b.to_host(name, slot) for b in self.blocks])
+            dist, dev = self._gather_dev()
+            blk = self.blocks[0]
+            t = blk.t[name] if slot is None else blk.t[name][slot]
+            blk.synchronize()
+            mine = t[:blk.m].to(dev)
+            lens = torch.zeros(self.P, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(lens, torch.tensor([blk.m], dtype=torch.int64,
+                                                           device=dev))
+            lens = lens.tolist()
+            mx = max(lens)
+            buf = torch.zeros(mx, dtype=torch.float64, device=dev)
+            buf[:blk.m] = mine
+            out = torch.empty(self.P * mx, dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(out, buf)
+            out = out.view(self.P, mx).cpu().numpy()
+            return np.concatenate([out[g, :lens[g]] for g in range(self.P)])
         # owned columns of rank g = slab g of every chunk: a (K, P, cw) view of
         # the padded vector, so the pieces move by strided copies, not fancy indexing
-        k, cw, _ = self._col_layout()
+        k, cw, npad = self._col_layout()
         if self.P == 1:
             return self.blocks[0].to_host(name, slot)
-        pieces = []
+        if self.nccl:
+            dist, dev = self._gather_dev()
+            blk = self.blocks[0]
+            t = blk.t[name] if slot is None else blk.t[name][slot]
+            blk.synchronize()
+            pad = torch.zeros(k * self.P * cw, dtype=torch.float64, device=t.device)
+            ln = min(t.numel(), pad.numel())
+            pad[:ln] = t[:ln]
+            mine = pad.view(k, self.P, cw)[:, self.rank0, :].contiguous().to(dev)
+            got = torch.empty((self.P, k, cw), dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(got, mine)
+            return got.permute(1, 0, 2).reshape(-1)[:self.n].cpu().numpy()
+        out = np.empty(k * self.P * cw)
+        slabs = out.reshape(k, self.P, cw)
         for l, b in enumerate(self.blocks):
             pad = np.zeros(k * self.P * cw)
             v = b.to_host(name, slot)
             pad[:v.size] = v
             g = self.rank0 + l
-            pieces.append((g, pad.reshape(k, self.P, cw)[:, g, :].copy()))
-        if self.nccl:
-            import torch.distributed as dist
-            got = [None] * self.P
-            dist.all_gather_object(got, pieces[0])
-            pieces = got
-        out = np.empty(k * self.P * cw)
-        slabs = out.reshape(k, self.P, cw)
-        for g, vals in pieces:
-            slabs[:, g, :] = vals
+            slabs[:, g, :] = pad.reshape(k, self.P, cw)[:, g, :]
         return out[:self.n]
 
     def close(self):
@@ -345,6 +372,43 @@ def broadcast_nccl_id(rank: int) -> bytes:
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+class _BlockShell:
+    """What ``solve`` reads from the problem when the device object is a
+    row-block group: the objective constant and sense (problem.py:22-36)."""
+
+    def __init__(self, objective_constant=0.0, objective_negated=False):
+        self.objective_constant = float(objective_constant)
+        self.objective_negated = bool(objective_negated)
+
+
+def solve_row_block(block, cfg=None, *, n, m_total, m1_total, nnz_total, row0,
+                    objective_constant: float = 0.0, objective_negated: bool = False,
+                    device: int | None = None):
+    """One rank per process (torch.distributed initialised by the caller), each
+    rank passing ONLY its own row block -- ``block`` = (row_offsets,
+    col_indices, values, m1_local, b, c, lower, upper) of rows [row0, row0 +
+    m_g) of the stacked A = [A_eq; A_ineq] -- for problems no single host
+    holds.  The report is the whole problem's on every rank (the row-block
+    path of ``solve``)."""
+    import os
+    import torch.distributed as dist
+    from .driver import solve
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(), dist.get_world_size()
+        nid = broadcast_nccl_id(rank)
+    else:                                        # a one-rank job (NCCL world of 1)
+        rank, world, nid = 0, 1, nccl_unique_id()
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    grp = RowBlockGroup.distributed(block, n=n, m_total=m_total, m1_total=m1_total,
+                                    nnz_total=nnz_total, row0=row0, rank=rank, world=world,
+                                    nccl_id=nid, device=device)
+    try:
+        return solve(_BlockShell(objective_constant, objective_negated), cfg, dev=grp)
+    finally:
+        grp.close()
 
 
 def solve_distributed(problem, cfg=None, *, device: int | None = None):
