@@ -362,7 +362,7 @@ def _build_reports(pk: PackedBatch, raw, lraw, x, y, z, max_log: int = MAX_LOG) 
     return out
 
 
-PIPE_CHUNK = 1024      # LPs per pipelined launch (solve_batch on large batches)
+PIPE_CHUNK = 512       # LPs per pipelined launch (C5 sweep: 4096 / 2048 / 1024 / 512 / 256 -> 217 / 157 / 140 / 133 / 137 ms per call)
 PIPE_MIN = 2048        # batches smaller than this run as one launch
 
 

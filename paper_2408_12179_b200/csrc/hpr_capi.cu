@@ -108,7 +108,7 @@ int64_t windows_of(int64_t nrows) { return (nrows + kWindow - 1) / kWindow; }
 
 // per-matrix plan arrays in the main workspace
 struct PlanOff {
-  size_t slice_row, slice_len, slice_slots, slice_ptr, slice_base, long_flag, long_rows, nsel;
+  size_t slice_row, slice_len, slice_slots, slice_ptr, long_flag, long_rows, nsel;
 };
 
 // column-blocked (CB) engine plan arrays of one matrix (persistent, workspace)
@@ -262,10 +262,9 @@ Layout make_layout(const hpr_dims &d, size_t cub_bytes) {
     p.slice_len = take(sizeof(unsigned short) * nw * kWindow);
     p.slice_slots = take(sizeof(int) * (ns + 1));
     p.slice_ptr = take(sizeof(int) * (ns + 1));
-    p.slice_base = take(sizeof(int) * ns);
     p.long_flag = take(sizeof(int) * nrows);
     p.long_rows = take(sizeof(int) * nrows);
-    p.nsel = take(sizeof(int));
+    p.nsel = take(2 * sizeof(int));   // [selected long rows, compact slice prefix]
     return p;
   };
   L.pa = plan(d.m);
@@ -348,12 +347,12 @@ struct Sell {
   int nrows = 0, nslices = 0, nlong = 0;
   long long slots = 0;
   unsigned short *slice_len = nullptr;
-  int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *slice_base = nullptr,
-      *long_flag = nullptr,
+  int *slice_row = nullptr, *slice_slots = nullptr, *slice_ptr = nullptr, *long_flag = nullptr,
       *long_rows = nullptr, *nsel = nullptr;
   int *ci = nullptr, *pos = nullptr;
   double *val_s = nullptr, *val0 = nullptr;
   bool affinity = false;   // rows in the row-affinity order (row_affinity_order)
+  int compact = 0;         // leading compact slices (SellMat::compact)
 };
 
 }  // namespace
@@ -431,7 +430,7 @@ struct hpr_ctx {
   SellMat mat(const Sell &S, const int *rp, const int *ci, const double *csr_val, bool scaled) const {
     const int ga = S.nslices > 0 && S.slots >= (long long)HPR_GA_MIN * 32 * S.nslices;
     return SellMat{S.slice_ptr, S.slice_row, S.slice_len, S.ci, scaled ? S.val_s : S.val0, rp, ci, csr_val,
-                   S.long_rows, S.nslices, S.nlong, ga, 0, HPR_COMPACT_HDR ? S.slice_base : nullptr};
+                   S.long_rows, S.nslices, S.nlong, ga, 0, HPR_COMPACT_HDR ? S.compact : 0};
   }
   CbMat cbmat(const Cb &C, int ncols) const {
     return CbMat{C.row_start, C.gseg, C.rpb, C.rpb_base, C.ci, C.val, C.G, C.NB, kCbW, ncols,
@@ -612,20 +611,21 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   S.slice_len = (unsigned short *)(c->ws + po.slice_len);
   S.slice_slots = (int *)(c->ws + po.slice_slots);
   S.slice_ptr = (int *)(c->ws + po.slice_ptr);
-  S.slice_base = (int *)(c->ws + po.slice_base);
   S.long_flag = (int *)(c->ws + po.long_flag);
   S.long_rows = (int *)(c->ws + po.long_rows);
   S.nsel = (int *)(c->ws + po.nsel);
   cudaStream_t s = c->stream;
   CK(cudaMemsetAsync(S.slice_slots + S.nslices, 0, sizeof(int), s));
+  k_fill_int<<<1, 1, 0, s>>>(S.nsel + 1, 1, S.nslices);   // compact prefix: min over slices
+  CKL();
   if (win == kSortWinBig)
     k_sell_plan<kSortWinBig><<<(nrows + win - 1) / win, win, 0, s>>>(
         rp, nrows, 1, S.slice_row, S.slice_len, S.slice_slots, S.long_flag, long_thresh, m_pad,
-        m_real, order, S.slice_base);
+        m_real, order, S.nsel + 1);
   else
     k_sell_plan<kWindow><<<nw, kWindow, 0, s>>>(rp, nrows, 1, S.slice_row, S.slice_len,
                                                 S.slice_slots, S.long_flag, long_thresh, m_pad,
-                                                m_real, order, S.slice_base);
+                                                m_real, order, S.nsel + 1);
   S.affinity = order != nullptr;
   CKL();
   size_t tb = c->L.cub_bytes;
@@ -635,13 +635,14 @@ int plan_sell(hpr_ctx *c, const PlanOff &po, const int *rp, int nrows, Sell &S,
   CK(cub::DeviceSelect::Flagged(c->ws + c->L.cub_tmp, tb, cub::CountingInputIterator<int>(0),
                                 S.long_flag, S.long_rows, S.nsel, nrows, s));
   c->launches += 3;
-  int total = 0, nl = 0;
+  int total = 0, nl[2] = {0, 0};
   CK(cudaMemcpyAsync(&total, S.slice_ptr + S.nslices, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&nl, S.nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(nl, S.nsel, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (total < 0) return fail(HPR_EINVAL, "SELL slot count overflows int32");
   S.slots = total;
-  S.nlong = nl;
+  S.nlong = nl[0];
+  S.compact = (m_pad == 0 && !order) ? nl[1] : 0;
   return HPR_OK;
 }
 
@@ -1049,6 +1050,97 @@ int kkt_common(hpr_ctx *c, int term_original, int slot, hpr_ckpt_out *out) {
   rc = fetch_results(c);
   if (rc) return rc;
   fill_out(c, out);
+  return HPR_OK;
+}
+
+}  // namespace
+
+#include "hpr_small.cuh"
+
+namespace {
+
+// ---- resident small-LP inner loop (hpr_small.cuh) ----
+// Cluster size for the resident loop, or 0 for the graph path: used when both
+// SELL layouts have <= kSmallMaxWin windows (HPR_SMALL=0 disables it,
+// HPR_SMALL=1 forces it whenever a cluster can be launched).
+int small_cluster(hpr_ctx *c) {
+  const char *env = getenv("HPR_SMALL");
+  if (env && env[0] == '0') return 0;
+  // the staged / column-blocked / column-split engines are large-problem
+  // layouts: when one is on (forced), the graph path runs it
+  if (!(env && env[0] == '1') && (c->sta.on || c->stat.on || c->cba.on || c->cbat.on || c->sp.on))
+    return 0;
+  const int wa = (c->sa.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int wat = (c->sat.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int wmax = std::max(wa, wat);
+  if (!(env && env[0] == '1') && wmax > kSmallMaxWin) return 0;
+  int G = std::max(1, std::min(kSmallMaxCluster, wmax));
+  return G;
+}
+
+template <bool GAX, bool GAY>
+int launch_small(hpr_ctx *c, int G, const SellMat &AT, const SellMat &A, const EpiXIter &ex,
+                 const EpiYIter &ey, int steps) {
+  auto kern = k_small_inner<GAX, GAY>;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int &o = g_attr[{(const void *)kern, c->device}];
+    if (o == 0) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      o = 1;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, AT, A, (const double *)c->B.y, (const double *)c->B.w, ex, ey,
+                        steps, (int)HPR_X_IMPLICIT));
+  CKL();
+  return HPR_OK;
+}
+
+int run_small(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, double lamsig,
+              int variant) {
+  const hpr_buffers &B = c->B;
+  cudaStream_t s = c->stream;
+  const SellMat A = c->mat_a(true), AT = c->mat_at(true);
+  EpiXIter ex{};
+  ex.c = B.c_s;
+  ex.lo = B.lower_s;
+  ex.up = B.upper_s;
+  ex.bounds_uniform = c->bounds_uniform;
+  ex.lo_u = c->lo_u;
+  ex.up_u = c->up_u;
+  ex.anc = B.anc_x;
+  ex.x = B.x;
+  ex.w = B.w;
+  ex.P = c->params;
+  EpiYIter ey{};
+  ey.b = B.b_s;
+  ey.anc = B.anc_y;
+  ey.y = B.y;
+  ey.P = c->params;
+  ey.m1 = (int)c->d.m1;
+  const int G = small_cluster(c);
+  k_set_params<<<1, 1, 0, s>>>(c->params, sigma, lamsig, (long long)t, (long long)k, variant);
+  CKL();
+  CK(cudaEventRecord(c->ev0, s));
+  int rc = AT.ga ? (A.ga ? launch_small<true, true>(c, G, AT, A, ex, ey, steps)
+                         : launch_small<true, false>(c, G, AT, A, ex, ey, steps))
+                 : (A.ga ? launch_small<false, true>(c, G, AT, A, ex, ey, steps)
+                         : launch_small<false, false>(c, G, AT, A, ex, ey, steps));
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev1, s));
+  c->inner_timed = true;
+  c->launches += 2;
   return HPR_OK;
 }
 
@@ -1579,6 +1671,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
   if (steps <= 0) return HPR_OK;
   if (variant < 0 || variant > 2) return fail(HPR_EINVAL, "bad variant");
   CK(cudaSetDevice(c->device));
+  if (small_cluster(c) > 0) return run_small(c, steps, t, k, sigma, lamsig, variant);
   const hpr_buffers &B = c->B;
   cudaStream_t s = c->stream;
   auto it = c->inner_graphs.find(steps);

@@ -86,6 +86,20 @@ __device__ __forceinline__ double ld_gather(const double *ptr) {
 #endif
 }
 
+// Gathers of a vector other CTAs of the same launch write (the resident
+// small-LP loop, hpr_small.cuh): a weak coherent load -- ordered after the
+// cluster barrier's acquire -- never the non-coherent path.
+__device__ __forceinline__ double ld_coherent(const double *ptr) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(ptr) : "memory");
+  return v;
+}
+template <bool COH>
+__device__ __forceinline__ double gather(const double *ptr) {
+  if constexpr (COH) return ld_coherent(ptr);
+  else return ld_gather(ptr);
+}
+
 // Row operands of the iteration epilogues (read once per iteration): with
 // HPR_EPI_NA they bypass L1 allocation so the gathered vector keeps the L1.
 #ifndef HPR_EPI_NA
@@ -124,10 +138,11 @@ struct SellMat {
   int nlong;
   int ga;                  // long rows: gather one batch ahead (HPR_GA_MIN)
   int keep;                // L2 policy of the matrix streams: 0 evict_first, 1 evict_last, 2 normal
-  // nslices (or nullptr): b >= 0 marks a compact slice -- lane i owns row b + i
-  // and every row has the slice's length -- whose per-lane header
-  // (slice_row / slice_len, 6 bytes a row) is then never read; -1 otherwise
-  const int *slice_base;
+  // slices [0, compact) are compact: slice s holds rows 32 s .. 32 s + 31 (no
+  // reordering) all of the slice's length, so their per-lane header
+  // (slice_row / slice_len, 6 bytes a row) is never read -- the row follows
+  // from s and the lane, the length from slice_ptr
+  int compact;
 };
 
 constexpr int kSlice = 32;
@@ -232,9 +247,8 @@ __device__ __forceinline__ SliceHdr load_hdr(const SellMat &M, int s, int lane) 
   if (s < M.nslices) {
     h.base = M.slice_ptr[s];
     h.slen = (M.slice_ptr[s + 1] - h.base) / kSlice;
-    const int b = M.slice_base ? M.slice_base[s] : -1;
-    if (b >= 0) {
-      h.row = b + lane;
+    if (s < M.compact) {
+      h.row = s * kSlice + lane;
       h.len = h.slen;
     } else {
       h.row = M.slice_row[s * kSlice + lane];
@@ -260,7 +274,7 @@ template <class E>
 struct has_final<E, std::void_t<decltype(std::declval<E &>().final(nullptr, 0))>>
     : std::true_type {};
 
-template <int U, bool GA, class Epi>
+template <int U, bool GA, class Epi, bool COH = false>
 __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
@@ -290,7 +304,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
   double x0[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (u < len) x0[u] = ld_gather(xg + c[u]);
+    if (u < len) x0[u] = gather<COH>(xg + c[u]);
   int c1[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
@@ -301,7 +315,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + U + u < len) {
-        x1[u] = ld_gather(xg + c1[u]);
+        x1[u] = gather<COH>(xg + c1[u]);
         v1[u] = ld_stream(vp + (k + U + u) * kSlice, pol);
       }
 #pragma unroll
@@ -324,7 +338,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
   double x0[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (u < len) x0[u] = ld_gather(xg + c[u]);
+    if (u < len) x0[u] = gather<COH>(xg + c[u]);
   int c1[U];
   double v1[U];
 #pragma unroll
@@ -337,7 +351,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
     double x1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (k + U + u < len) x1[u] = ld_gather(xg + c1[u]);
+      if (k + U + u < len) x1[u] = gather<COH>(xg + c1[u]);
     int c2[U];
     double v2[U];
 #pragma unroll
@@ -369,7 +383,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (k + u < len) xv[u] = ld_gather(xg + c[u]);
+      if (k + u < len) xv[u] = gather<COH>(xg + c[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
@@ -387,7 +401,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 }
 
 // a long row: the warp forms 32 products at a time, lane 0 adds them in order
-template <class Epi>
+template <class Epi, bool COH = false>
 __device__ __forceinline__ void long_row(const SellMat &M, int row, int lane,
                                          const double *__restrict__ xg, Epi &epi, double *acc,
                                          uint64_t pol) {
@@ -397,7 +411,8 @@ __device__ __forceinline__ void long_row(const SellMat &M, int row, int lane,
   for (int c0 = z0; c0 < z1; c0 += 32) {
     const int kk = c0 + lane;
     double p = 0.0;
-    if (kk < z1) p = __dmul_rn(ld_stream(M.csr_val + kk, pol), __ldg(xg + ld_stream(M.csr_ci + kk, pol)));
+    if (kk < z1)
+      p = __dmul_rn(ld_stream(M.csr_val + kk, pol), gather<COH>(xg + ld_stream(M.csr_ci + kk, pol)));
     const int cnt = min(32, z1 - c0);
     for (int i = 0; i < cnt; ++i) {
       const double q = __shfl_sync(0xffffffffu, p, i);
@@ -946,7 +961,7 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
                                                    int *slice_row, unsigned short *slice_len,
                                                    int *slice_slots, int *long_flag,
                                                    int long_thresh, int m_pad, int m_real,
-                                                   const int *order, int *slice_base) {
+                                                   const int *order, int *compact_prefix) {
   __shared__ int key[WIN];
   __shared__ int skey[WIN];
   __shared__ int srow[WIN];
@@ -986,13 +1001,12 @@ __global__ void __launch_bounds__(WIN) k_sell_plan(const int *rp, int nrows, int
     int mx = 0;
     for (int i = 0; i < kSlice; ++i) mx = max(mx, skey[t * kSlice + i]);
     slice_slots[blockIdx.x * (WIN / kSlice) + t] = mx * kSlice;
-    // compact slice: 32 consecutive rows of equal length (no per-lane header)
-    const int r0 = srow[t * kSlice];
-    bool compact = r0 >= 0;
-    for (int i = 1; i < kSlice && compact; ++i)
-      compact = srow[t * kSlice + i] == r0 + i && skey[t * kSlice + i] == mx;
-    compact = compact && skey[t * kSlice] == mx;
-    slice_base[blockIdx.x * (WIN / kSlice) + t] = compact ? r0 : -1;
+    // compact slice: rows 32 s .. 32 s + 31 in place, all of equal length
+    const int sl = blockIdx.x * (WIN / kSlice) + t;
+    bool compact = true;
+    for (int i = 0; i < kSlice && compact; ++i)
+      compact = srow[t * kSlice + i] == sl * kSlice + i && skey[t * kSlice + i] == mx;
+    if (!compact) atomicMin(compact_prefix, sl);
   }
 }
 
@@ -1150,6 +1164,9 @@ __global__ void k_gather_vals(const int *perm, const double *src, double *dst, l
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
        k += (long long)gridDim.x * blockDim.x)
     dst[k] = src[perm[k]];
+}
+__global__ void k_fill_int(int *a, int n, int v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = v;
 }
 __global__ void k_fill(double *a, double v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;

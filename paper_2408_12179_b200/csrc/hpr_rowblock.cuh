@@ -394,7 +394,7 @@ int g_at_partial_chunk(hpr_group *g, int l, const double *v, int q) {
   M.slice_ptr += s0;
   M.slice_row += s0 * kSlice;
   M.slice_len += s0 * kSlice;
-  if (M.slice_base) M.slice_base += s0;
+  M.compact = 0;   // a compact slice's row is 32 s + lane in the unshifted numbering
   M.nslices = (int)std::max<long long>(0, std::min<long long>(g->CW / kSlice, M.nslices - s0));
   if (q > 0) M.nlong = 0;
   EpiStore es{};

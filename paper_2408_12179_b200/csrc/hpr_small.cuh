@@ -1,0 +1,69 @@
+// hpr_small.cuh -- the resident inner loop for small LPs (launch-latency path).
+//
+// Reference: run_inner / iterate_once (core.py:163-179).  For an LP whose
+// SELL layouts have at most kSmallMaxWin windows per matrix (C1: A^T 16, A 8
+// windows of 128 rows), the 2 x check_interval kernels of an interval's graph
+// are launch-latency bound (a few microseconds each, for a microsecond of
+// work).  Here ONE launch of one thread-block cluster (<= 16 CTAs, one per
+// SM) runs the whole interval: each CTA owns a fixed set of windows of A^T and
+// of A (the same static assignment as k_sell), and the two phases of every
+// iteration are separated by hardware cluster barriers
+// (barrier.cluster.arrive.release / wait.acquire) instead of kernel
+// boundaries.  The iterates y and w that other CTAs of the launch write are
+// gathered with weak coherent loads (ld_coherent), ordered by the barrier's
+// acquire; the matrix streams stay on the non-coherent path (read-only).
+//
+// The per-row arithmetic is the same sell_slice / long_row code and the same
+// EpiXIter / EpiYIter epilogues as the graph path, so the iterates are
+// bit-identical to it (tests/test_gpu_parity.py forces both).
+#pragma once
+
+namespace hpr {
+
+constexpr int kSmallMaxCluster = 16;   // non-portable cluster size limit on B200
+constexpr int kSmallMaxWin = 64;       // windows per matrix up to which the path is used
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <bool GA, class Epi>
+__device__ __forceinline__ void small_phase(const SellMat &M, const double *xg, Epi &epi,
+                                            uint64_t pol) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  double acc[1] = {0.0};
+  for (int win = blockIdx.x; win < nwin; win += G) {
+    const SliceHdr h = load_hdr(M, win * kWarpsPerCta + wib, lane);
+    sell_slice<GA ? 4 : HPR_SELL_U, GA, Epi, true>(M, h, lane, xg, epi, acc, pol);
+  }
+  for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += G * kWarpsPerCta)
+    long_row<Epi, true>(M, M.long_rows[li], lane, xg, epi, acc, pol);
+}
+
+// `steps` HPR iterations: x-phase over A^T (gathers y), barrier, y-phase over
+// A (gathers w), barrier.  x_implicit: HPR keeps x implicit between the first
+// and last step (EpiXIter).
+template <bool GAX, bool GAY>
+__global__ void __launch_bounds__(kThreads)
+k_small_inner(SellMat AT, SellMat A, const double *y, const double *w, EpiXIter ex, EpiYIter ey,
+              int steps, int x_implicit) {
+  const uint64_t pol = policy_evict_last();      // the whole LP stays in L2
+  for (int i = 0; i < steps; ++i) {
+    ex.step = i;
+    ex.x_from_w = x_implicit && i > 0;
+    ex.x_store = !x_implicit || i == steps - 1;
+    ex.enter();
+    small_phase<GAX>(AT, y, ex, pol);
+    cluster_barrier();
+    ey.step = i;
+    ey.enter();
+    small_phase<GAY>(A, w, ey, pol);
+    cluster_barrier();
+  }
+}
+
+}  // namespace hpr

@@ -109,11 +109,14 @@ def assert_report_parity(rep, g, name="", tol=1e-8):
 # split into blocks whose running sums are carried block to block
 # (HPR_SPLIT_COLS) / staged segmented engine (HPR_STG, both phases) / SELL
 # with both matrices' rows in the row-affinity order (HPR_RAO=1, 2^5-column
-# blocks so small problems get a non-trivial order)
-ENGINES = ["sell", "cb", "split", "stg", "rao"]
+# blocks so small problems get a non-trivial order) / the resident small-LP
+# loop (HPR_SMALL=1: one cluster launch per interval, hpr_small.cuh); every
+# other engine runs on the per-iteration graph path (HPR_SMALL=0)
+ENGINES = ["sell", "cb", "split", "stg", "rao", "small"]
 
 
 def _engine_env(monkeypatch, engine, n):
+    monkeypatch.setenv("HPR_SMALL", "1" if engine == "small" else "0")
     monkeypatch.setenv("HPR_CB", "1" if engine == "cb" else "0")
     monkeypatch.setenv("HPR_STG", "1" if engine == "stg" else "0")
     if engine == "rao":
@@ -492,3 +495,22 @@ def test_flow_lp_downscaled_vs_oracle():
     rep = P.solve(prob, P.SolverConfig(**cfg))
     ref = O.solve(O.OracleLP.from_problem(prob), O.OracleConfig(**cfg))
     assert_report_parity(rep, ref, "flow_lp_downscaled")
+
+
+def test_small_resident_loop_matches_graph_path(monkeypatch):
+    """The resident small-LP loop (one cluster launch per interval, default for
+    C1-size LPs) and the per-iteration graph path give the same solve: same
+    report, bit-identical solution."""
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    cfg = P.SolverConfig(tolerance=1e-8)
+    reps = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HPR_SMALL", mode)
+        reps[mode] = P.solve(prob, cfg)
+    a, b = reps["0"], reps["1"]
+    assert a.to_json_dict(False) | {"timings": None, "device_stats": None} == \
+        b.to_json_dict(False) | {"timings": None, "device_stats": None}
+    for f in "xyz":
+        assert np.array_equal(getattr(a.solution, f), getattr(b.solution, f))
+    # one launch per interval instead of 2 x check_interval
+    assert b.device_stats["launches"] < a.device_stats["launches"]
