@@ -201,6 +201,7 @@ typedef struct hpr_layout_info_t {
   int64_t rao_a, rao_at; /* 1: SELL rows in the row-affinity order (gathered vector > L2) */
   int64_t bounds_uniform; /* after hpr_scale: bit 0 every scaled lower bound equal, bit 1
                              every upper bound equal (passed as scalars, not streamed) */
+  int64_t ts_a, ts_at;   /* blocks of the bulk-copy-streamed (TS) iteration engine (0: off) */
 } hpr_layout_info_t;
 int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 

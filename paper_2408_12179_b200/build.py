@@ -9,13 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "hpr_capi.cu"), os.path.join(HERE, "csrc", "hpr_mps.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "hpr_kernels.cuh"),
-              os.path.join(HERE, "csrc", "hpr_cb.cuh"),
-              os.path.join(HERE, "csrc", "hpr_stg.cuh"),
-              os.path.join(HERE, "csrc", "hpr_rowblock.cuh"),
-              os.path.join(HERE, "csrc", "hpr_batch.cuh"),
-              os.path.join(HERE, "csrc", "hpr_exact.cuh"),
-              os.path.join(ROOT, "include", "hprlp_b200.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))
+              if f.endswith((".cuh", ".h"))] + [os.path.join(ROOT, "include", "hprlp_b200.h")]
 OUT = os.path.join(HERE, "libhprlp_b200.so")
 
 NVCC_FLAGS = [

@@ -21,6 +21,7 @@
 #include "hpr_kernels.cuh"
 #include "hpr_cb.cuh"
 #include "hpr_stg.cuh"
+#include "hpr_tsell.cuh"
 #include "hpr_exact.cuh"
 
 using namespace hpr;
@@ -53,6 +54,9 @@ int fail(int code, const std::string &msg) {
 #endif
 #ifndef HPR_CARVEOUT
 #define HPR_CARVEOUT -1   // SELL kernels' preferred shared-memory carve-out (-1: driver default)
+#endif
+#ifndef HPR_TS_DEFAULT
+#define HPR_TS_DEFAULT 2    // TS engine selection without HPR_TS: 0 never, 1 always, 2 auto
 #endif
 #ifndef HPR_L2KEEP
 #define HPR_L2KEEP 4    // matrix L2 policy: 0 evict_first, 1 keep A, 2 keep A^T, 3 normal, 4 auto
@@ -391,6 +395,12 @@ struct hpr_ctx {
     unsigned char *rec = nullptr;
   } sta, stat;
   const Stg *stg_sorted = nullptr;   // whose sorted items the STG temporaries hold
+  // TS engine (hpr_tsell.cuh) for the iteration phases: block cuts of A
+  // (ts_blk[0 .. ts_nb_a]) and A^T (ts_blk + ts_nb_a + 1), ctx-owned
+  int *ts_blk = nullptr;
+  size_t ts_cap = 0;
+  int ts_nb_a = 0, ts_nb_at = 0;
+  bool ts_a = false, ts_at = false;
   int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
@@ -740,6 +750,79 @@ int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *
   k_stg_fill<<<ng, 256, sh, s>>>(rp, ci, T.row_start, T.NB, (unsigned *)(c->ws + c->L.stg_skey),
                                  (int *)(c->ws + c->L.stg_slrow),
                                  (long long *)(c->ws + c->L.stg_gstart), T.goff, T.rec, T.pos);
+  CKL();
+  c->launches += 1;
+  return HPR_OK;
+}
+
+// TS engine for the iteration phases (hpr_tsell.cuh): HPR_TS=0 never, 1
+// whenever the SELL kernel would run, 2 (auto) when the matrix stream does not
+// fit in L2.  A matrix qualifies when its largest slice leaves a block target
+// T of at least a quarter of a stage.
+int ts_plan(hpr_ctx *c) {
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+  const char *env = getenv("HPR_TS");
+  const int mode_all = env ? atoi(env) : HPR_TS_DEFAULT;
+  cudaStream_t s = c->stream;
+  long long T[2] = {0, 0};
+  int nb[2] = {0, 0};
+  const Sell *SS[2] = {&c->sa, &c->sat};
+  const bool other[2] = {c->sp.on || c->sta.on || c->cba.on, c->stat.on || c->cbat.on};
+  for (int q = 0; q < 2; ++q) {
+    const Sell &S = *SS[q];
+    const char *em = getenv(q ? "HPR_TS_AT" : "HPR_TS_A");   // per-matrix override
+    const int mode = em ? atoi(em) : mode_all;
+    if (mode == 0 || S.nslices == 0 || other[q]) continue;
+    // auto: a matrix stream larger than L2 with short rows (<= 8 slots per lane
+    // on average).  C3 (us/iteration): A^T (3 per row) on TS 997 -> 870; A
+    // (10.7 per row, HBM gathers of w) on TS is slower (+52), so it stays on k_sell
+    if (mode != 1 && (12.0 * (double)S.slots <= (double)l2 || S.slots > 8LL * kSlice * S.nslices))
+      continue;
+    int *dmax = (int *)(c->ws + c->L.keys_out);   // scratch (free after the transpose)
+    size_t tb = c->L.cub_bytes;
+    CK(cub::DeviceReduce::Max(c->ws + c->L.cub_tmp, tb, S.slice_slots, dmax, S.nslices, s));
+    int mx = 0;
+    CK(cudaMemcpyAsync(&mx, dmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->launches += 1;
+    const long long t = (long long)kTsCap - mx - kTsSw;
+    if (t < kTsCap / 4) continue;
+    T[q] = t;
+    nb[q] = (int)((S.slots + (long long)kTsSw * S.nslices + t - 1) / t);
+  }
+  const size_t need = (size_t)(nb[0] + 1) + (size_t)(nb[1] + 1);
+  bool changed = (T[0] > 0) != c->ts_a || (T[1] > 0) != c->ts_at || nb[0] != c->ts_nb_a ||
+                 nb[1] != c->ts_nb_at;
+  if (need > c->ts_cap) {
+    if (c->ts_blk) CK(cudaFree(c->ts_blk));
+    c->ts_blk = nullptr;
+    c->ts_cap = 0;
+    CK(cudaMalloc(&c->ts_blk, sizeof(int) * need));
+    c->ts_cap = need;
+    changed = true;
+  }
+  if (T[0] > 0)
+    k_ts_plan<<<(nb[0] + 256) / 256, 256, 0, s>>>(c->sa.slice_ptr, c->sa.nslices, T[0], nb[0],
+                                                   c->ts_blk);
+  if (T[1] > 0)
+    k_ts_plan<<<(nb[1] + 256) / 256, 256, 0, s>>>(c->sat.slice_ptr, c->sat.nslices, T[1], nb[1],
+                                                   c->ts_blk + nb[0] + 1);
+  CKL();
+  c->launches += (int)(T[0] > 0) + (int)(T[1] > 0);
+  if (changed) c->drop_inner_graphs();
+  c->ts_a = T[0] > 0;
+  c->ts_at = T[1] > 0;
+  c->ts_nb_a = nb[0];
+  c->ts_nb_at = nb[1];
+  return HPR_OK;
+}
+
+template <class Epi>
+int launch_ts(hpr_ctx *c, const SellMat &M, const int *blk, int nblk, const double *xg,
+              const Epi &epi) {
+  if (int e = ensure_dyn_smem(k_tsell<HPR_TS_U, Epi>, kTsSmem)) return e;
+  k_tsell<HPR_TS_U, Epi><<<c->num_sms, kTsThreads, kTsSmem, c->stream>>>(M, xg, epi, blk, nblk);
   CKL();
   c->launches += 1;
   return HPR_OK;
@@ -1197,6 +1280,7 @@ int hpr_ctx_destroy(hpr_ctx *c) {
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_params) cudaFreeHost(c->h_params);
   if (c->h_pow) cudaFreeHost(c->h_pow);
+  if (c->ts_blk) cudaFree(c->ts_blk);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
@@ -1383,6 +1467,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
       default: break;
     }
   }
+  rc = ts_plan(c);
+  if (rc) return rc;
   c->laid_out = true;
   c->scaled = false;
   return HPR_OK;
@@ -1707,10 +1793,12 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
       // the first kernel of the graph follows the k_set_params launch: plain edge
       int rc2 = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
                 : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
+                : c->ts_at ? launch_ts(c, AT, c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, B.y, ex)
                              : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
       if (!rc2)
         rc2 = c->sta.on ? launch_stg(c, c->sta, (int)c->d.n, B.w, ey)
               : c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
+              : c->ts_a ? launch_ts(c, A, c->ts_blk, c->ts_nb_a, B.w, ey)
                           : launch_a_iter(c, B.w, ey, true);
       if (rc2) {
         c->l2win_active = false;
@@ -1880,6 +1968,8 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->rao_a = c->sa.affinity;
   info->rao_at = c->sat.affinity;
   info->bounds_uniform = c->bounds_uniform;
+  info->ts_a = c->ts_a ? c->ts_nb_a : 0;
+  info->ts_at = c->ts_at ? c->ts_nb_at : 0;
   return HPR_OK;
 }
 

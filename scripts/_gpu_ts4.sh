@@ -1,0 +1,13 @@
+#!/bin/bash
+# TS variants on C3: both phases on TS, the x-phase only (A^T), the y-phase only, per variant.
+mkdir -p gpurun_out
+out=gpurun_out/ts_var.log; : > $out
+for so in paper_2408_12179_b200/libhprlp_b200.so paper_2408_12179_b200/variants/*.so; do
+  for m in "1 1" "0 1" "1 0"; do
+    set -- $m
+    echo "== $(basename $so) HPR_TS_A=$1 HPR_TS_AT=$2" >> $out
+    HPR_LIB_PATH=$PWD/$so HPR_TS_A=$1 HPR_TS_AT=$2 timeout 120 python scripts/prof_iter.py --config c3 --reps 3 2>&1 | grep per-iter >> $out
+  done
+done
+echo "== off" >> $out
+HPR_TS=0 timeout 120 python scripts/prof_iter.py --config c3 --reps 3 2>&1 | grep per-iter >> $out

@@ -111,12 +111,14 @@ def assert_report_parity(rep, g, name="", tol=1e-8):
 # with both matrices' rows in the row-affinity order (HPR_RAO=1, 2^5-column
 # blocks so small problems get a non-trivial order) / the resident small-LP
 # loop (HPR_SMALL=1: one cluster launch per interval, hpr_small.cuh); every
-# other engine runs on the per-iteration graph path (HPR_SMALL=0)
-ENGINES = ["sell", "cb", "split", "stg", "rao", "small"]
+# other engine runs on the per-iteration graph path (HPR_SMALL=0) / the
+# bulk-copy-streamed SELL engine on both phases (HPR_TS=1, hpr_tsell.cuh)
+ENGINES = ["sell", "cb", "split", "stg", "rao", "small", "ts"]
 
 
 def _engine_env(monkeypatch, engine, n):
     monkeypatch.setenv("HPR_SMALL", "1" if engine == "small" else "0")
+    monkeypatch.setenv("HPR_TS", "1" if engine == "ts" else "0")
     monkeypatch.setenv("HPR_CB", "1" if engine == "cb" else "0")
     monkeypatch.setenv("HPR_STG", "1" if engine == "stg" else "0")
     if engine == "rao":
@@ -144,6 +146,7 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert info["split_a"] == (7 if engine == "split" else 0)
     assert (info["stg_a"] > 0 and info["stg_at"] > 0) == (engine == "stg")
     assert (info["rao_a"], info["rao_at"]) == ((1, 1) if engine == "rao" else (0, 0))
+    assert (info["ts_a"] > 0 and info["ts_at"] > 0) == (engine == "ts")
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.83, lam,
@@ -162,7 +165,7 @@ def test_iteration_bit_exact_c1(variant, code, engine, monkeypatch):
     assert np.array_equal(dev.to_host("x"), st.x)
 
 
-@pytest.mark.parametrize("engine", ["sell", "split", "stg", "rao"])
+@pytest.mark.parametrize("engine", ["sell", "split", "stg", "rao", "ts"])
 def test_iteration_bit_exact_midsize(engine, monkeypatch):
     """140k x 140k, 7 per row: >= 131072 rows (the HPR_SORT_WIN threshold) and
     the column-split A over seven 20k-column blocks."""
@@ -172,6 +175,7 @@ def test_iteration_bit_exact_midsize(engine, monkeypatch):
     info = dev.layout_info()
     assert info["split_a"] == (7 if engine == "split" else 0)
     assert (info["stg_a"], info["stg_at"]) == ((18, 18) if engine == "stg" else (0, 0))
+    assert (info["ts_a"] > 0 and info["ts_at"] > 0) == (engine == "ts")
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.7, lam)
