@@ -87,11 +87,14 @@ def load_traffic(config):
 
 def iteration_kernels(lay):
     """Names of the two iteration kernels the layout selected."""
-    x = "k_stg<EpiXIter>" if lay.get("stg_at") else "k_sell<EpiXIter>"
+    x = ("k_stg<EpiXIter>" if lay.get("stg_at") else
+         "k_tsell<EpiXIter>" if lay.get("ts_at") else "k_sell<EpiXIter>")
     if lay.get("stg_a"):
         y = "k_stg<EpiYIter>"
     elif lay.get("split_a"):
         y = f"{lay['split_a']} x k_sell<EpiCarry..> (column-split)"
+    elif lay.get("ts_a"):
+        y = "k_tsell<EpiYIter>"
     else:
         y = "k_sell<EpiYIter>"
     return f"{x} + {y} (one HPR iteration)"

@@ -401,6 +401,10 @@ struct hpr_ctx {
   size_t ts_cap = 0;
   int ts_nb_a = 0, ts_nb_at = 0;
   bool ts_a = false, ts_at = false;
+  // row-block column chunks of A^T (slices per chunk, 0: one range): the A^T
+  // plan is then cut per chunk, chunk q = blocks [ts_at_off[q], ts_at_off[q+1])
+  int ts_chunk_sl = 0;
+  std::vector<int> ts_at_off;
   int num_sms = 148;
   double *part = nullptr, *results = nullptr, *fac = nullptr, *dvec_m = nullptr, *dvec_n = nullptr;
   IterParams *params = nullptr;
@@ -775,9 +779,12 @@ int ts_plan(hpr_ctx *c) {
     const int mode = em ? atoi(em) : mode_all;
     if (mode == 0 || S.nslices == 0 || other[q]) continue;
     // auto: a matrix stream larger than L2 with short rows (<= 8 slots per lane
-    // on average).  C3 (us/iteration): A^T (3 per row) on TS 997 -> 870; A
-    // (10.7 per row, HBM gathers of w) on TS is slower (+52), so it stays on k_sell
-    if (mode != 1 && (12.0 * (double)S.slots <= (double)l2 || S.slots > 8LL * kSlice * S.nslices))
+    // on average), mostly in compact slices.  C3 (us/iteration): A^T (3 per
+    // row, compact) on TS 997 -> 849; A (10.7 per row, HBM gathers of w) on TS
+    // is slower (+52); C4's A_g^T (6.25 per row, sigma-sorted, 28 % padding)
+    // too (1668 -> 1896 us per rank iteration): both stay on k_sell
+    if (mode != 1 && (12.0 * (double)S.slots <= (double)l2 || S.slots > 8LL * kSlice * S.nslices ||
+                      2LL * S.compact < S.nslices))
       continue;
     int *dmax = (int *)(c->ws + c->L.keys_out);   // scratch (free after the transpose)
     size_t tb = c->L.cub_bytes;
@@ -791,9 +798,34 @@ int ts_plan(hpr_ctx *c) {
     T[q] = t;
     nb[q] = (int)((S.slots + (long long)kTsSw * S.nslices + t - 1) / t);
   }
+  // A^T in chunks (row-block overlap path): block counts per chunk from the
+  // chunk boundaries' slot offsets
+  std::vector<int> off_at(2, 0), lo_at(1, 0), hi_at(1, c->sat.nslices);
+  if (T[1] > 0) {
+    const Sell &S = c->sat;
+    const int cs = c->ts_chunk_sl > 0 ? c->ts_chunk_sl : S.nslices;
+    const int kc = (S.nslices + cs - 1) / cs;
+    std::vector<int> bnd(kc + 1);
+    for (int q = 0; q <= kc; ++q) bnd[q] = std::min(S.nslices, q * cs);
+    std::vector<int> sp(kc + 1);
+    for (int q = 0; q <= kc; ++q)
+      CK(cudaMemcpyAsync(&sp[q], S.slice_ptr + bnd[q], sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    off_at.assign(kc + 1, 0);
+    lo_at.assign(kc, 0);
+    hi_at.assign(kc, 0);
+    for (int q = 0; q < kc; ++q) {
+      const long long wq = (long long)(sp[q + 1] - sp[q]) + (long long)kTsSw * (bnd[q + 1] - bnd[q]);
+      const int nq = bnd[q + 1] > bnd[q] ? (int)((wq + T[1] - 1) / T[1]) : 0;
+      off_at[q + 1] = off_at[q] + nq + 1;   // + 1: the range's end entry
+      lo_at[q] = bnd[q];
+      hi_at[q] = bnd[q + 1];
+    }
+    nb[1] = off_at[kc] - 1;   // whole-matrix launches: one list (the end entries are empty blocks)
+  }
   const size_t need = (size_t)(nb[0] + 1) + (size_t)(nb[1] + 1);
   bool changed = (T[0] > 0) != c->ts_a || (T[1] > 0) != c->ts_at || nb[0] != c->ts_nb_a ||
-                 nb[1] != c->ts_nb_at;
+                 nb[1] != c->ts_nb_at || off_at != c->ts_at_off;
   if (need > c->ts_cap) {
     if (c->ts_blk) CK(cudaFree(c->ts_blk));
     c->ts_blk = nullptr;
@@ -803,18 +835,23 @@ int ts_plan(hpr_ctx *c) {
     changed = true;
   }
   if (T[0] > 0)
-    k_ts_plan<<<(nb[0] + 256) / 256, 256, 0, s>>>(c->sa.slice_ptr, c->sa.nslices, T[0], nb[0],
+    k_ts_plan<<<(nb[0] + 256) / 256, 256, 0, s>>>(c->sa.slice_ptr, 0, c->sa.nslices, T[0], nb[0],
                                                    c->ts_blk);
   if (T[1] > 0)
-    k_ts_plan<<<(nb[1] + 256) / 256, 256, 0, s>>>(c->sat.slice_ptr, c->sat.nslices, T[1], nb[1],
-                                                   c->ts_blk + nb[0] + 1);
+    for (size_t q = 0; q + 1 < off_at.size(); ++q) {
+      const int nq = off_at[q + 1] - off_at[q] - 1;
+      k_ts_plan<<<(nq + 256) / 256, 256, 0, s>>>(c->sat.slice_ptr, lo_at[q], hi_at[q], T[1], nq,
+                                                  c->ts_blk + nb[0] + 1 + off_at[q]);
+      c->launches += 1;
+    }
   CKL();
-  c->launches += (int)(T[0] > 0) + (int)(T[1] > 0);
+  c->launches += (int)(T[0] > 0);
   if (changed) c->drop_inner_graphs();
   c->ts_a = T[0] > 0;
   c->ts_at = T[1] > 0;
   c->ts_nb_a = nb[0];
   c->ts_nb_at = nb[1];
+  c->ts_at_off = off_at;
   return HPR_OK;
 }
 

@@ -382,6 +382,8 @@ int g_at_partial(hpr_group *g, int l, bool scaled, const double *v, const PowSta
   EpiStore es{};
   es.out = g->r[l].xpart;
   es.S = gate;
+  if (scaled && c->ts_at && c->ts_chunk_sl == 0)   // TS engine (iteration x-phase)
+    return launch_ts(c, c->mat_at(true), c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, v, es);
   return launch_sell(c, c->mat_at(scaled), v, es, nullptr, nullptr);
 }
 
@@ -389,6 +391,16 @@ int g_at_partial(hpr_group *g, int l, bool scaled, const double *v, const PowSta
 // windows); the long rows ride with chunk 0 so they precede every reduction
 int g_at_partial_chunk(hpr_group *g, int l, const double *v, int q) {
   hpr_ctx *c = g->r[l].c;
+  if (c->ts_at && c->ts_chunk_sl == g->CW / kSlice && q + 1 < (int)c->ts_at_off.size()) {
+    // TS engine over chunk q's own blocks (global slice ids; long rows with chunk 0)
+    SellMat M = c->mat_at(true);
+    if (q > 0) M.nlong = 0;
+    EpiStore es{};
+    es.out = g->r[l].xpart;
+    es.S = nullptr;
+    const int o = c->ts_at_off[q], nq = c->ts_at_off[q + 1] - o - 1;
+    return launch_ts(c, M, c->ts_blk + c->ts_nb_a + 1 + o, nq, v, es);
+  }
   SellMat M = c->mat_at(true);
   const long long s0 = (long long)q * g->CW / kSlice;
   M.slice_ptr += s0;
@@ -566,6 +578,15 @@ int hpr_group_create(hpr_group **out, int nlocal, hpr_ctx *const *ctxs, void *co
   rb_dims(n, nranks, chunks, &g->cw, &g->npad);
   g->CW = g->cw * nranks;
   g->stream = ctxs[0]->stream;
+  if (use_nccl && chunks > 1)   // the overlapped x-phase launches A^T chunk by chunk: TS plan per chunk
+    for (int l = 0; l < nlocal; ++l) {
+      ctxs[l]->ts_chunk_sl = (int)(g->CW / kSlice);
+      cudaSetDevice(ctxs[l]->device);
+      if (int rc = ts_plan(ctxs[l])) {
+        delete g;
+        return rc;
+      }
+    }
   g->use_nccl = use_nccl;
   {
     const char *force = getenv("HPR_RB_NCCL_P1");

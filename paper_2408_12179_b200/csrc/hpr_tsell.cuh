@@ -56,19 +56,21 @@ constexpr int kTsOffLen = kTsOffRow + kTsMaxSl * kSlice * 4;
 constexpr int kTsStageBytes = (kTsOffLen + kTsMaxSl * kSlice * 2 + 127) & ~127;
 constexpr int kTsSmem = kTsStages * kTsStageBytes;
 
-// Block b = slices [blk[b], blk[b+1]): cut where the weight slice_ptr[s] +
-// kTsSw s crosses a multiple of T (T + the largest slice + kTsSw <= kTsCap,
-// checked by the host), so a block holds <= kTsCap slots and <= T / kTsSw + 1
-// slices; empty slices cost weight too.
-__global__ void k_ts_plan(const int *slice_ptr, int nslices, long long T, int nblk, int *blk) {
+// Block b = slices [blk[b], blk[b+1]) of the slice range [s_lo, s_hi): cut
+// where the weight slice_ptr[s] + kTsSw s crosses base + b T (T + the largest
+// slice + kTsSw <= kTsCap, checked by the host), so a block holds <= kTsCap
+// slots and <= T / kTsSw + 1 slices; empty slices cost weight too.  Ranges let
+// the row-block path plan each column chunk on its own (no block straddles one).
+__global__ void k_ts_plan(const int *slice_ptr, int s_lo, int s_hi, long long T, int nblk,
+                          int *blk) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > nblk) return;
   if (b == nblk) {
-    blk[b] = nslices;
+    blk[b] = s_hi;
     return;
   }
-  const long long target = T * b;
-  int a = 0, z = nslices;
+  const long long target = (long long)slice_ptr[s_lo] + (long long)kTsSw * s_lo + T * b;
+  int a = s_lo, z = s_hi;
   while (a < z) {
     const int mid = (a + z) >> 1;
     if ((long long)slice_ptr[mid] + (long long)kTsSw * mid < target) a = mid + 1; else z = mid;

@@ -49,6 +49,8 @@ class _Staging:
 
 
 _POOL = None
+_PF_POOL = None
+_BIG_SOLUTION = 32 << 20   # solution bytes from which the staged download pays off
 
 
 def _par_copy(dst, src):
@@ -331,6 +333,49 @@ class DeviceLP:
             t = t[:self.n]
         self.stream.synchronize()
         return t.cpu().numpy()
+
+    def prefault_solution(self):
+        """Start allocating the solution arrays (y[m], z[n], x[n]) on a host
+        thread and touch their pages while the solve runs: a fresh 268 MB
+        array costs ~0.1 s of page faults when the D2H copy first writes it
+        (C3: 285 of 4460 ms per solve).  None for small problems."""
+        if 8 * (self.m + 2 * self.n) < _BIG_SOLUTION:
+            return None
+        global _PF_POOL
+        if _PF_POOL is None:
+            import concurrent.futures
+            _PF_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=1)
+
+        def alloc(m, n):
+            out = (np.empty(m), np.empty(n), np.empty(n))
+            for a in out:
+                a.fill(0.0)
+            return out
+        return _PF_POOL.submit(alloc, self.m, self.n)
+
+    def solution_to_host(self, slot, prefault=None):
+        """(y, z, x) of candidate slot ``slot`` as fresh numpy arrays: one D2H
+        of the three vectors into the pinned staging buffer, then a threaded
+        copy into the arrays ``prefault`` prepared (pages already touched)."""
+        m, n = self.m, self.n
+        total = 8 * (m + 2 * n)
+        if total < _BIG_SOLUTION:
+            return tuple(self.to_host(nm, slot) for nm in ("cand_y", "cand_z", "cand_x"))
+        torch = _torch()
+        with _Staging.lock:
+            st = _Staging.get(total)[:total].view(torch.float64)
+            with torch.cuda.stream(self.stream):
+                st[:m].copy_(self.t["cand_y"][slot][:m], non_blocking=True)
+                st[m:m + n].copy_(self.t["cand_z"][slot][:n], non_blocking=True)
+                st[m + n:].copy_(self.t["cand_x"][slot][:n], non_blocking=True)
+            out = prefault.result() if prefault is not None else (np.empty(m), np.empty(n),
+                                                                   np.empty(n))
+            self.stream.synchronize()
+            src = st.numpy()
+            _par_copy(out[0], src[:m])
+            _par_copy(out[1], src[m:m + n])
+            _par_copy(out[2], src[m + n:])
+        return out
 
     def close(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:

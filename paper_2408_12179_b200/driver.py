@@ -387,6 +387,8 @@ def _solve(problem, cfg, dev) -> SolveReport:
     variant = cfg.variant
     vcode = N.VARIANT_CODE[variant.value]
 
+    prefault = getattr(dev, "prefault_solution", None)
+    prefault = prefault() if prefault is not None else None   # solution arrays, off-thread
     t0 = time.perf_counter()
     if not dev.analyzed:
         dev.analyze()
@@ -494,9 +496,11 @@ def _solve(problem, cfg, dev) -> SolveReport:
     dobj += objective_constant
     if objective_negated:
         pobj, dobj = -pobj, -dobj
-    solution = PrimalDualPoint(y=dev.to_host("cand_y", final_slot),
-                               z=dev.to_host("cand_z", final_slot),
-                               x=dev.to_host("cand_x", final_slot))
+    if hasattr(dev, "solution_to_host"):
+        sy, sz, sx = dev.solution_to_host(final_slot, prefault)
+    else:
+        sy, sz, sx = (dev.to_host(nm, final_slot) for nm in ("cand_y", "cand_z", "cand_x"))
+    solution = PrimalDualPoint(y=sy, z=sz, x=sx)
     layout = dev.layout_info()
     return SolveReport(
         status=status, primal_objective=pobj, dual_objective=dobj, kkt=res, iterations=k,

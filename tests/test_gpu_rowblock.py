@@ -32,9 +32,12 @@ def _traj_rel(y, x, ry, rx):
         np.sum(ry ** 2) + np.sum(rx ** 2))
 
 
-@pytest.mark.parametrize("parts,chunks", [(1, 1), (2, 1), (3, 1), (5, 1), (2, 3), (4, 2)])
-def test_partitioned_trajectory_c1(parts, chunks, monkeypatch):
+@pytest.mark.parametrize("parts,chunks,ts", [(1, 1, 0), (2, 1, 0), (3, 1, 0), (5, 1, 0), (2, 3, 0),
+                                             (4, 2, 0), (1, 1, 1), (3, 1, 1)])
+def test_partitioned_trajectory_c1(parts, chunks, ts, monkeypatch):
+    """ts = 1: every rank's A_g^T partial (and y-phase) on the TS engine."""
     monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
+    monkeypatch.setenv("HPR_TS", str(ts))
     d = np.load(f"{GOLDEN}/c1_golden.npz")
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     grp = RowBlockGroup.local(prob, parts)
@@ -159,12 +162,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("chunks", [1, 3])
-def test_nccl_transport_world1(golden_reports, chunks, monkeypatch):
+@pytest.mark.parametrize("chunks,ts", [(1, 0), (3, 0), (1, 1), (3, 1)])
+def test_nccl_transport_world1(golden_reports, chunks, ts, monkeypatch):
     """chunks > 1 runs the overlapped pipeline (comm stream, per-chunk events,
     chunked NCCL reduce-scatter / all-gather) -- with one rank the collectives
-    are copies, but the captured multi-stream graph is the P-GPU one."""
+    are copies, but the captured multi-stream graph is the P-GPU one.  ts = 1:
+    the A^T partial on the TS engine, planned per column chunk when chunked."""
     monkeypatch.setenv("HPR_RB_CHUNKS", str(chunks))
+    monkeypatch.setenv("HPR_TS", str(ts))
     monkeypatch.setenv("HPR_RB_NCCL_P1", "1")      # keep the NCCL collectives at one rank
     import torch
     import torch.distributed as dist
