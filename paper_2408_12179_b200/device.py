@@ -336,10 +336,13 @@ class DeviceLP:
 
     def prefault_solution(self):
         """Start allocating the solution arrays (y[m], z[n], x[n]) on a host
-        thread and touch their pages while the solve runs: a fresh 268 MB
-        array costs ~0.1 s of page faults when the D2H copy first writes it
-        (C3: 285 of 4460 ms per solve).  None for small problems."""
-        if 8 * (self.m + 2 * self.n) < _BIG_SOLUTION:
+        thread and touch their pages while the solve runs (a fresh 268 MB
+        array costs ~0.1 s of page faults when first written).  None for small
+        problems and unless HPR_PREFAULT=1."""
+        import os
+        # opt-in (HPR_PREFAULT=1): C3 solution_to_host 35 -> 24 ms, but the
+        # faulting thread slowed the next upload / teardown of e2e solves
+        if 8 * (self.m + 2 * self.n) < _BIG_SOLUTION or os.environ.get("HPR_PREFAULT") != "1":
             return None
         global _PF_POOL
         if _PF_POOL is None:
@@ -356,7 +359,9 @@ class DeviceLP:
     def solution_to_host(self, slot, prefault=None):
         """(y, z, x) of candidate slot ``slot`` as fresh numpy arrays: one D2H
         of the three vectors into the pinned staging buffer, then a threaded
-        copy into the arrays ``prefault`` prepared (pages already touched)."""
+        copy into new arrays (the page faults spread over the copy threads) or
+        into the ones ``prefault`` prepared.  C3: 35 ms, against 285 ms for
+        three torch ``.cpu()`` downloads into fresh pageable arrays."""
         m, n = self.m, self.n
         total = 8 * (m + 2 * n)
         if total < _BIG_SOLUTION:

@@ -308,10 +308,10 @@ class _DevicePool:
     is checked out for the duration of a solve, so concurrent solves never
     share one."""
 
-    def __init__(self, capacity: int = 2, max_bytes: float = 4e9):
+    def __init__(self, capacity: int = 2, max_bytes: float | None = None):
         import threading
         self.capacity = capacity
-        self.max_bytes = max_bytes
+        self.max_bytes = max_bytes   # None: a quarter of the device's memory (B200: ~45 GB)
         self.free: list[DeviceLP] = []
         self.lock = threading.Lock()
 
@@ -330,7 +330,11 @@ class _DevicePool:
         return dev
 
     def release(self, dev: DeviceLP):
-        if 92 * dev.nnz + 160 * (dev.m + dev.n) > self.max_bytes:
+        limit = self.max_bytes
+        if limit is None:
+            import torch
+            limit = 0.25 * torch.cuda.get_device_properties(dev.device).total_memory
+        if 92 * dev.nnz + 160 * (dev.m + dev.n) > limit:
             dev.close()                       # large residencies are not kept
             return
         with self.lock:
