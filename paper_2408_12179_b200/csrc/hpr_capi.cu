@@ -846,7 +846,13 @@ int ts_plan(hpr_ctx *c) {
     }
   CKL();
   c->launches += (int)(T[0] > 0);
-  if (changed) c->drop_inner_graphs();
+  if (changed) {   // the captured inner-loop and power graphs hold the plan
+    c->drop_inner_graphs();
+    if (c->pow_graph) {
+      cudaGraphExecDestroy(c->pow_graph);
+      c->pow_graph = nullptr;
+    }
+  }
   c->ts_a = T[0] > 0;
   c->ts_at = T[1] > 0;
   c->ts_nb_a = nb[0];
@@ -1699,11 +1705,12 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < kPowBatch; ++i) {
       int ga = 0;
-      if (c->stat.on) {
+      if (c->stat.on || c->ts_at) {   // u = A^T v without the (unused) norm partials
         EpiPowTu eu{};
         eu.u = u;
         eu.S = c->pow;
-        rc = launch_stg(c, c->stat, (int)c->d.m, v, eu);
+        rc = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, v, eu)
+                        : launch_ts(c, c->mat_at(true), c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, v, eu);
       } else {
         rc = launch_sell(c, c->mat_at(true), v, et, P.powt, nullptr);
       }

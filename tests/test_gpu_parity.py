@@ -501,6 +501,28 @@ def test_flow_lp_downscaled_vs_oracle():
     assert_report_parity(rep, ref, "flow_lp_downscaled")
 
 
+@pytest.mark.parametrize("ts", ["0", "1"])
+def test_flow_lp_compact_many_blocks_bit_exact(ts, monkeypatch):
+    """A flow LP large enough that every TS CTA walks many blocks of compact
+    A^T slices (2 M columns, ~14 blocks per CTA): the cross-block look-ahead of
+    the row operands and the per-block ring phases, bit-exact vs the oracle."""
+    monkeypatch.setenv("HPR_TS", ts)
+    prob = P.generate_flow_lp(5, nodes=1 << 14, out_degree=4, commodities=32)
+    dev = _dev(prob)
+    info = dev.layout_info()
+    assert (info["ts_a"] > 0 and info["ts_at"] > 0) == (ts == "1")
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    slp = _oracle_on_device_scaling(dev, prob)
+    st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 1.0, lam)
+    dev.state_reset()
+    for k in range(12):
+        dev.run_inner(1, k, k, 1.0, lam, 2)
+        O.iterate_once(st, slp)
+        assert np.array_equal(dev.to_host("y"), st.y), k
+        assert np.array_equal(dev.to_host("x"), st.x), k
+    dev.close()
+
+
 def test_small_resident_loop_matches_graph_path(monkeypatch):
     """The resident small-LP loop (one cluster launch per interval, default for
     C1-size LPs) and the per-iteration graph path give the same solve: same
