@@ -865,7 +865,8 @@ template <class Epi>
 int launch_ts(hpr_ctx *c, const SellMat &M, const int *blk, int nblk, const double *xg,
               const Epi &epi) {
   if (int e = ensure_dyn_smem(k_tsell<HPR_TS_U, Epi>, kTsSmem)) return e;
-  k_tsell<HPR_TS_U, Epi><<<c->num_sms, kTsThreads, kTsSmem, c->stream>>>(M, xg, epi, blk, nblk);
+  k_tsell<HPR_TS_U, Epi><<<c->num_sms * kTsCps, kTsThreads, kTsSmem, c->stream>>>(M, xg, epi, blk,
+                                                                                  nblk);
   CKL();
   c->launches += 1;
   return HPR_OK;

@@ -41,6 +41,10 @@ namespace hpr {
 #ifndef HPR_TS_SW
 #define HPR_TS_SW 32         // plan weight of a slice (bounds the slices per block; C3: 32 849, 64 863, 128 (4 stages) 878 us/iteration)
 #endif
+#ifndef HPR_TS_CPS
+#define HPR_TS_CPS 1         // persistent CTAs per SM
+#endif
+constexpr int kTsCps = HPR_TS_CPS;
 constexpr int kTsWarps = HPR_TS_WARPS;
 constexpr int kTsThreads = (kTsWarps + 1) * 32;
 constexpr int kTsCap = HPR_TS_CAP;
@@ -79,7 +83,7 @@ __global__ void k_ts_plan(const int *slice_ptr, int s_lo, int s_hi, long long T,
 }
 
 template <int U, class Epi>
-__global__ void __launch_bounds__(kTsThreads, 1)
+__global__ void __launch_bounds__(kTsThreads, kTsCps)
 k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict__ blk, int nblk) {
   static_assert(Epi::NQ == 0, "TS engine: iteration epilogues only");
   extern __shared__ __align__(128) unsigned char ts_sm[];
