@@ -529,6 +529,10 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
 #if HPR_BATCH_PROF
   tp_pow = clock64();
 #endif
+#ifndef HPR_BATCH_REG
+#define HPR_BATCH_REG 1
+#endif
+  const bool reg = HPR_BATCH_REG && n <= 2 * kBT && m <= kBT;
   while (status < 0) {
 #if HPR_BATCH_PROF
     const long long tq0 = clock64();
@@ -537,6 +541,81 @@ __global__ void __launch_bounds__(kBT, 1) k_batch_solve(Prob P, Cfg C, Out O) {
     const double lamsig = lamv * sigma;
     bool broke = false;
     const long long t_seg = t;
+    if (reg) {
+      // register-resident interval (HPR_BATCH_REG): thread tid owns columns
+      // tid, tid + kBT and row tid for the whole interval, so x and the
+      // column / row constants (c, l, u, anchors, b) stay in registers; only
+      // the gathered vectors (w, y) go through shared memory.  Same operations
+      // in the same order as the loop below: bit-identical.
+      const int j0 = tid < n ? tid : -1, j1 = tid + kBT < n ? tid + kBT : -1;
+      const int qr = tid < m ? tid : -1;
+      double xr0 = 0.0, xr1 = 0.0, cr0 = 0.0, cr1 = 0.0, lr0 = 0.0, lr1 = 0.0, ur0 = 0.0,
+             ur1 = 0.0, ar0 = 0.0, ar1 = 0.0, yr = 0.0, br = 0.0, ayr = 0.0;
+      bool ineq = false;
+      if (j0 >= 0) { xr0 = x[j0]; cr0 = cs[j0]; lr0 = ls[j0]; ur0 = us[j0]; ar0 = ax[j0]; }
+      if (j1 >= 0) { xr1 = x[j1]; cr1 = cs[j1]; lr1 = ls[j1]; ur1 = us[j1]; ar1 = ax[j1]; }
+      if (qr >= 0) { yr = y[qr]; br = bs[qr]; ayr = ay[qr]; ineq = aperm[qr] >= m1; }
+      for (long long st = 0; st < steps; ++st) {
+        if (st % kWTab == 0) {
+          for (int q = tid; q < kWTab; q += kBT) {
+            const double tq = (double)(t_seg + st + q);
+            const double t2 = tq + 2.0;          // core.py:142-144
+            wtab[2 * q] = (tq + 1.0) / t2;
+            wtab[2 * q + 1] = 1.0 / t2;
+          }
+          __syncthreads();
+        }
+        const double wn = wtab[2 * (st % kWTab)], wa = wtab[2 * (st % kWTab) + 1];
+        int bad = 0;
+        if (j0 >= 0) {                           // x phase (core.py:168-169)
+          double aty0, aty1;
+          srow2(atst, atlen, atci, atv, y, j0, j1, aty0, aty1);
+          {
+            const double v = __dadd_rn(xr0, __dmul_rn(sigma, __dsub_rn(aty0, cr0)));
+            const double xbj = np_clip(v, lr0, ur0);
+            const double wj = __dsub_rn(__dmul_rn(2.0, xbj), xr0);
+            const double xn = C.variant == 0 ? xbj
+                              : __dadd_rn(__dmul_rn(wa, ar0), __dmul_rn(wn, C.variant == 2 ? wj : xbj));
+            w[j0] = wj;
+            xr0 = xn;
+            bad |= !isfinite(xn);
+          }
+          if (j1 >= 0) {
+            const double v = __dadd_rn(xr1, __dmul_rn(sigma, __dsub_rn(aty1, cr1)));
+            const double xbj = np_clip(v, lr1, ur1);
+            const double wj = __dsub_rn(__dmul_rn(2.0, xbj), xr1);
+            const double xn = C.variant == 0 ? xbj
+                              : __dadd_rn(__dmul_rn(wa, ar1), __dmul_rn(wn, C.variant == 2 ? wj : xbj));
+            w[j1] = wj;
+            xr1 = xn;
+            bad |= !isfinite(xn);
+          }
+        }
+        __syncthreads();
+        if (qr >= 0) {                           // y phase (core.py:170-172)
+          const double s2 = srow(ast, alen, aci, av, w, qr);
+          double ybi = __dadd_rn(yr, __ddiv_rn(__dsub_rn(br, s2), lamsig));
+          if (ineq) ybi = np_max(ybi, 0.0);
+          double yn = ybi;
+          if (C.variant != 0) {
+            const double tg = C.variant == 2 ? __dsub_rn(__dmul_rn(2.0, ybi), yr) : ybi;
+            yn = __dadd_rn(__dmul_rn(wa, ayr), __dmul_rn(wn, tg));
+          }
+          y[qr] = yn;
+          yr = yn;
+          bad |= !isfinite(yn);
+        }
+        if (__syncthreads_or(bad)) {
+          broke = true;
+          break;
+        }
+        ++t;
+        ++k;
+      }
+      if (j0 >= 0) x[j0] = xr0;
+      if (j1 >= 0) x[j1] = xr1;
+      __syncthreads();
+    } else
     for (long long st = 0; st < steps; ++st) {
       if (st % kWTab == 0) {                     // Halpern weights of the next kWTab steps
         for (int q = tid; q < kWTab; q += kBT) {
