@@ -91,8 +91,17 @@ class PackedBatch:
             for (k, dt), nb in zip(self.ORDER, nbs):
                 out[k] = buf[o:o + nb].view(dt)
                 o += (nb + 255) // 256 * 256
+        host = _host_module()
         if os.environ.get("HPR_PACK_LOOP") == "1":
             rp, ci, val, b, c, lo, up = self._pack_loop(problems, ns, nzs)
+        elif host is not None and os.environ.get("HPR_PACK_NATIVE", "1") == "1":
+            for k, dt in self.ORDER:                 # the native packer writes these in place
+                if k in ("rp", "ci", "val", "b", "c", "lower", "upper") and k not in out:
+                    out[k] = np.empty(lens[k], dt)
+            host.pack_batch(problems, out, self.row_off, self.col_off, self.nz_off,
+                            min(8, os.cpu_count() or 1))
+            rp, ci, val, b, c, lo, up = (out[k] for k in ("rp", "ci", "val", "b", "c", "lower",
+                                                          "upper"))
         else:
             rp, ci, val, b, c, lo, up = self._pack_concat(problems, out)
         self.arrays = {
@@ -170,6 +179,22 @@ class PackedBatch:
 
     def h2d_bytes(self):
         return sum(a.nbytes for a in self.arrays.values())
+
+
+_HOST = False
+
+
+def _host_module():
+    """The native host helpers (csrc/hpr_host.cpp, built in-tree by build.py),
+    or None -- batch packing then runs in numpy."""
+    global _HOST
+    if _HOST is False:
+        try:
+            from . import _hpr_host
+            _HOST = _hpr_host
+        except ImportError:
+            _HOST = None
+    return _HOST
 
 
 def _config(cfg: SolverConfig, max_log: int) -> N.HprBatchConfig:

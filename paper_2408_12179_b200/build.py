@@ -37,12 +37,41 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
+HOST_SRC = os.path.join(HERE, "csrc", "hpr_host.cpp")
+
+
+def host_out() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_hpr_host" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_host(force: bool = False, verbose: bool = False) -> str | None:
+    """The pybind11 host helpers (batch packing), g++ in-tree; None when the
+    Python headers or pybind11 are unavailable (solve_batch then packs in numpy)."""
+    import sysconfig
+    try:
+        import pybind11
+    except ImportError:
+        return None
+    out = host_out()
+    if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(HOST_SRC):
+        return out
+    cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared", "-fPIC", "-pthread",
+           "-I" + sysconfig.get_paths()["include"], "-I" + pybind11.get_include(),
+           "-o", out, HOST_SRC]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SRC]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
+    build_host(force, verbose)
     return OUT
 
 
