@@ -397,8 +397,9 @@ struct hpr_ctx {
   const Stg *stg_sorted = nullptr;   // whose sorted items the STG temporaries hold
   // TS engine (hpr_tsell.cuh) for the iteration phases: block cuts of A
   // (ts_blk[0 .. ts_nb_a]) and A^T (ts_blk + ts_nb_a + 1), ctx-owned
-  int *ts_blk = nullptr;
-  size_t ts_cap = 0;
+  int *ts_blk = nullptr;               // in the caller's layout buffer (ts_bytes)
+  long long ts_T[2] = {0, 0};          // block weight targets (0: TS off for A / A^T)
+  long long ts_cap_n[2] = {0, 0};      // reserved list entries
   int ts_nb_a = 0, ts_nb_at = 0;
   bool ts_a = false, ts_at = false;
   // row-block column chunks of A^T (slices per chunk, 0: one range): the A^T
@@ -762,18 +763,22 @@ int stg_layout(hpr_ctx *c, char *&p, hpr_ctx::Stg &T, const int *rp, const int *
 // TS engine for the iteration phases (hpr_tsell.cuh): HPR_TS=0 never, 1
 // whenever the SELL kernel would run, 2 (auto) when the matrix stream does not
 // fit in L2.  A matrix qualifies when its largest slice leaves a block target
-// T of at least a quarter of a stage.
-int ts_plan(hpr_ctx *c) {
+// T of at least a quarter of a stage.  ts_select (hpr_analyze) decides and
+// sizes the block lists -- they live in the caller's layout buffer -- and
+// ts_plan (hpr_bind_layout, and again when a row-block group cuts A^T into
+// column chunks) fills them.
+constexpr int kTsMaxChunks = 64;   // A^T column chunks the reserved block list covers
+int ts_select(hpr_ctx *c) {
   int l2 = 0;
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
   const char *env = getenv("HPR_TS");
   const int mode_all = env ? atoi(env) : HPR_TS_DEFAULT;
   cudaStream_t s = c->stream;
-  long long T[2] = {0, 0};
-  int nb[2] = {0, 0};
   const Sell *SS[2] = {&c->sa, &c->sat};
   const bool other[2] = {c->sp.on || c->sta.on || c->cba.on, c->stat.on || c->cbat.on};
   for (int q = 0; q < 2; ++q) {
+    c->ts_T[q] = 0;
+    c->ts_cap_n[q] = 0;
     const Sell &S = *SS[q];
     const char *em = getenv(q ? "HPR_TS_AT" : "HPR_TS_A");   // per-matrix override
     const int mode = em ? atoi(em) : mode_all;
@@ -786,7 +791,7 @@ int ts_plan(hpr_ctx *c) {
     if (mode != 1 && (12.0 * (double)S.slots <= (double)l2 || S.slots > 8LL * kSlice * S.nslices ||
                       2LL * S.compact < S.nslices))
       continue;
-    int *dmax = (int *)(c->ws + c->L.keys_out);   // scratch (free after the transpose)
+    int *dmax = (int *)c->part;   // scratch: no partials are live during analysis
     size_t tb = c->L.cub_bytes;
     CK(cub::DeviceReduce::Max(c->ws + c->L.cub_tmp, tb, S.slice_slots, dmax, S.nslices, s));
     int mx = 0;
@@ -795,15 +800,34 @@ int ts_plan(hpr_ctx *c) {
     c->launches += 1;
     const long long t = (long long)kTsCap - mx - kTsSw;
     if (t < kTsCap / 4) continue;
-    T[q] = t;
-    nb[q] = (int)((S.slots + (long long)kTsSw * S.nslices + t - 1) / t);
+    c->ts_T[q] = t;
+    const long long nb = (S.slots + (long long)kTsSw * S.nslices + t - 1) / t;
+    // entries: nb + 1 for one range; per column chunk at most one more block
+    // and one end entry each (A^T in the row-block overlap path)
+    c->ts_cap_n[q] = nb + 1 + (q ? 2LL * kTsMaxChunks : 0);
   }
+  return HPR_OK;
+}
+
+size_t ts_bytes(const hpr_ctx *c) {
+  return align_up(sizeof(int) * (size_t)(c->ts_cap_n[0] + c->ts_cap_n[1]) + 16, 256);
+}
+
+int ts_plan(hpr_ctx *c) {
+  cudaStream_t s = c->stream;
+  const long long *T = c->ts_T;
+  int nb[2] = {0, 0};
+  if (T[0] > 0) nb[0] = (int)((c->sa.slots + (long long)kTsSw * c->sa.nslices + T[0] - 1) / T[0]);
   // A^T in chunks (row-block overlap path): block counts per chunk from the
   // chunk boundaries' slot offsets
   std::vector<int> off_at(2, 0), lo_at(1, 0), hi_at(1, c->sat.nslices);
   if (T[1] > 0) {
     const Sell &S = c->sat;
-    const int cs = c->ts_chunk_sl > 0 ? c->ts_chunk_sl : S.nslices;
+    int cs = c->ts_chunk_sl > 0 ? c->ts_chunk_sl : S.nslices;
+    if ((S.nslices + cs - 1) / cs > kTsMaxChunks) {   // not reserved: whole-matrix plan only
+      c->ts_chunk_sl = 0;
+      cs = S.nslices;
+    }
     const int kc = (S.nslices + cs - 1) / cs;
     std::vector<int> bnd(kc + 1);
     for (int q = 0; q <= kc; ++q) bnd[q] = std::min(S.nslices, q * cs);
@@ -822,18 +846,10 @@ int ts_plan(hpr_ctx *c) {
       hi_at[q] = bnd[q + 1];
     }
     nb[1] = off_at[kc] - 1;   // whole-matrix launches: one list (the end entries are empty blocks)
+    if (off_at[kc] > c->ts_cap_n[1]) return fail(HPR_EINVAL, "TS block list exceeds its reservation");
   }
-  const size_t need = (size_t)(nb[0] + 1) + (size_t)(nb[1] + 1);
-  bool changed = (T[0] > 0) != c->ts_a || (T[1] > 0) != c->ts_at || nb[0] != c->ts_nb_a ||
-                 nb[1] != c->ts_nb_at || off_at != c->ts_at_off;
-  if (need > c->ts_cap) {
-    if (c->ts_blk) CK(cudaFree(c->ts_blk));
-    c->ts_blk = nullptr;
-    c->ts_cap = 0;
-    CK(cudaMalloc(&c->ts_blk, sizeof(int) * need));
-    c->ts_cap = need;
-    changed = true;
-  }
+  const bool changed = (T[0] > 0) != c->ts_a || (T[1] > 0) != c->ts_at || nb[0] != c->ts_nb_a ||
+                       nb[1] != c->ts_nb_at || off_at != c->ts_at_off;
   if (T[0] > 0)
     k_ts_plan<<<(nb[0] + 256) / 256, 256, 0, s>>>(c->sa.slice_ptr, 0, c->sa.nslices, T[0], nb[0],
                                                    c->ts_blk);
@@ -1324,7 +1340,6 @@ int hpr_ctx_destroy(hpr_ctx *c) {
   if (c->h_results) cudaFreeHost(c->h_results);
   if (c->h_params) cudaFreeHost(c->h_params);
   if (c->h_pow) cudaFreeHost(c->h_pow);
-  if (c->ts_blk) cudaFree(c->ts_blk);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
@@ -1434,7 +1449,9 @@ int hpr_analyze(hpr_ctx *c, size_t *layout_bytes) {
   if (rc) return rc;
   rc = stg_plan(c, c->L.sat, B.at_rp, B.at_ci, n, c->stat);
   if (rc) return rc;
-  *layout_bytes = sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz) +
+  rc = ts_select(c);
+  if (rc) return rc;
+  *layout_bytes = ts_bytes(c) + sell_bytes(c->sa, d.nnz) + sell_bytes(c->sat, d.nnz) +
                   cb_bytes(c->cba, d.nnz) + cb_bytes(c->cbat, d.nnz) + split_bytes(c->sp, d.nnz) +
                   stg_bytes(c->sta, d.nnz) + stg_bytes(c->stat, d.nnz);
   c->analyzed = true;
@@ -1447,7 +1464,7 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (rc) return rc;
   if (!c->analyzed) return fail(HPR_ESTATE, "hpr_analyze has not been called");
   if (!layout) return fail(HPR_EINVAL, "null layout");
-  if (bytes < sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz) +
+  if (bytes < ts_bytes(c) + sell_bytes(c->sa, c->d.nnz) + sell_bytes(c->sat, c->d.nnz) +
                   cb_bytes(c->cba, c->d.nnz) + cb_bytes(c->cbat, c->d.nnz) +
                   split_bytes(c->sp, c->d.nnz) + stg_bytes(c->sta, c->d.nnz) +
                   stg_bytes(c->stat, c->d.nnz))
@@ -1455,6 +1472,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   CK(cudaSetDevice(c->device));
   const hpr_buffers &B = c->B;
   char *p = (char *)layout;
+  c->ts_blk = (int *)p;   // TS block lists (filled by ts_plan below)
+  p += ts_bytes(c);
   rc = layout_sell(c, p, c->sa, B.a_rp, B.a_ci, B.a_val);
   if (rc) return rc;
   rc = layout_sell(c, p, c->sat, B.at_rp, B.at_ci, B.at_val);
