@@ -877,6 +877,16 @@ int ts_plan(hpr_ctx *c) {
   return HPR_OK;
 }
 
+// the TS x-phase streams its row operands and results evict-first (compact
+// slices: whole warp segments), so the gathered y keeps the L2 (HPR_TS_EF)
+#ifndef HPR_TS_EF
+#define HPR_TS_EF 1
+#endif
+EpiXIter ts_ef(EpiXIter e) {
+  e.ef = HPR_TS_EF;
+  return e;
+}
+
 template <class Epi>
 int launch_ts(hpr_ctx *c, const SellMat &M, const int *blk, int nblk, const double *xg,
               const Epi &epi) {
@@ -1857,7 +1867,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
       // the first kernel of the graph follows the k_set_params launch: plain edge
       int rc2 = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
                 : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
-                : c->ts_at ? launch_ts(c, AT, c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, B.y, ex)
+                : c->ts_at ? launch_ts(c, AT, c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, B.y, ts_ef(ex))
                              : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
       if (!rc2)
         rc2 = c->sta.on ? launch_stg(c, c->sta, (int)c->d.n, B.w, ey)

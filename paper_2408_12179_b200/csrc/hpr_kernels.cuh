@@ -105,6 +105,17 @@ __device__ __forceinline__ double gather(const double *ptr) {
 #ifndef HPR_EPI_NA
 #define HPR_EPI_NA 0
 #endif
+// evict-first streaming access of a row operand (TS x-phase: whole 256-byte
+// warp segments, nothing shared between warps) -- the gathered vector keeps L2
+__device__ __forceinline__ double ld_ef(const double *ptr, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_ef(double *ptr, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ double ld_epi(const double *ptr) {
 #if HPR_EPI_NA
   double v;
@@ -541,10 +552,13 @@ struct EpiXIter {
   int step;
   int bounds_uniform;        // bit 0: every lower bound equals lo_u, bit 1: upper / up_u
   int x_from_w = 0, x_store = 1;
+  int ef = 0;                // row operands / results streamed evict-first (TS engine)
   double lo_u, up_u;
   double sigma, wa, wn, wa0, wn0, xj, cj, lj, uj, aj;
   int variant, implicit;
+  uint64_t pol;
   __device__ bool enter() {
+    if (ef) pol = policy_evict_first();
     sigma = P->sigma;
     variant = P->variant;
     halpern_weights(P->t0 + step, wa, wn);
@@ -552,12 +566,13 @@ struct EpiXIter {
     if (implicit) halpern_weights(P->t0 + step - 1, wa0, wn0);
     return true;
   }
+  __device__ double ld(const double *p) const { return ef ? ld_ef(p, pol) : ld_epi(p); }
   __device__ void prefetch(int j) {
-    xj = ld_epi(implicit ? w + j : x + j);
-    cj = ld_epi(c + j);
-    lj = (bounds_uniform & 1) ? lo_u : ld_epi(lo + j);
-    uj = (bounds_uniform & 2) ? up_u : ld_epi(up + j);
-    aj = variant ? ld_epi(anc + j) : 0.0;
+    xj = ld(implicit ? w + j : x + j);
+    cj = ld(c + j);
+    lj = (bounds_uniform & 1) ? lo_u : ld(lo + j);
+    uj = (bounds_uniform & 2) ? up_u : ld(up + j);
+    aj = variant ? ld(anc + j) : 0.0;
   }
   __device__ void finish(int j, double aty, double *) {
     if (implicit) xj = __dadd_rn(__dmul_rn(wa0, aj), __dmul_rn(wn0, xj));   // x_k from w_{k-1}
@@ -566,8 +581,13 @@ struct EpiXIter {
     const double wj = __dsub_rn(__dmul_rn(2.0, xb), xj);
     const double xn =
         variant == 0 ? xb : __dadd_rn(__dmul_rn(wa, aj), __dmul_rn(wn, variant == 2 ? wj : xb));
-    w[j] = wj;
-    if (x_store || variant != 2) x[j] = xn;
+    if (ef) {
+      st_ef(w + j, wj, pol);
+      if (x_store || variant != 2) st_ef(x + j, xn, pol);
+    } else {
+      w[j] = wj;
+      if (x_store || variant != 2) x[j] = xn;
+    }
     if (!isfinite(xn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
   }
 };
