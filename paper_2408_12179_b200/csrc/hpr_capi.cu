@@ -882,6 +882,9 @@ int ts_plan(hpr_ctx *c) {
 #ifndef HPR_TS_EF
 #define HPR_TS_EF 1
 #endif
+#ifndef HPR_Y_EF
+#define HPR_Y_EF 1
+#endif
 EpiXIter ts_ef(EpiXIter e) {
   e.ef = HPR_TS_EF;
   return e;
@@ -1854,6 +1857,7 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
     ey.y = B.y;
     ey.P = c->params;
     ey.m1 = (int)c->d.m1;
+    ey.ef = HPR_Y_EF && c->ts_at;   // with the TS x-phase (HBM-bound problems)
     cudaGraph_t g;
     const long long before = c->launches;
     if (int e2 = l2_window_setup(c)) return e2;

@@ -599,18 +599,22 @@ struct EpiYIter {
   double *y;
   IterParams *P;
   int step, m1;
+  int ef = 0;                // row operands / results streamed evict-first
   double lamsig, wa, wn, yi, bi, ai;
   int variant;
+  uint64_t pol;
   __device__ bool enter() {
+    if (ef) pol = policy_evict_first();
     lamsig = P->lamsig;
     variant = P->variant;
     halpern_weights(P->t0 + step, wa, wn);
     return true;
   }
+  __device__ double ld(const double *p) const { return ef ? ld_ef(p, pol) : ld_epi(p); }
   __device__ void prefetch(int i) {
-    yi = ld_epi(y + i);
-    bi = ld_epi(b + i);
-    ai = variant ? ld_epi(anc + i) : 0.0;
+    yi = ld(y + i);
+    bi = ld(b + i);
+    ai = variant ? ld(anc + i) : 0.0;
   }
   __device__ void finish(int i, double s, double *) {
     double yb = __dadd_rn(yi, __ddiv_rn(__dsub_rn(bi, s), lamsig));
@@ -620,7 +624,8 @@ struct EpiYIter {
       const double tgt = variant == 2 ? __dsub_rn(__dmul_rn(2.0, yb), yi) : yb;
       yn = __dadd_rn(__dmul_rn(wa, ai), __dmul_rn(wn, tgt));
     }
-    y[i] = yn;
+    if (ef) st_ef(y + i, yn, pol);
+    else y[i] = yn;
     if (!isfinite(yn)) atomicMin(&P->nonfinite_k, (unsigned long long)(P->k0 + step));
   }
 };
