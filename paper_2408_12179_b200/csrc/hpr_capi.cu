@@ -886,7 +886,9 @@ int ts_plan(hpr_ctx *c) {
 #define HPR_Y_EF 1
 #endif
 EpiXIter ts_ef(EpiXIter e) {
-  e.ef = HPR_TS_EF;
+  // walking the blocks last to first (HPR_TS_REV), the w written last is the
+  // start of the y-phase's gather order: kept (normal stores), not evict-first
+  e.ef = HPR_TS_EF ? (HPR_TS_REV ? 1 : 3) : 0;
   return e;
 }
 

@@ -552,7 +552,7 @@ struct EpiXIter {
   int step;
   int bounds_uniform;        // bit 0: every lower bound equals lo_u, bit 1: upper / up_u
   int x_from_w = 0, x_store = 1;
-  int ef = 0;                // row operands / results streamed evict-first (TS engine)
+  int ef = 0;                // bit 0: row operands, bit 1: results streamed evict-first (TS engine)
   double lo_u, up_u;
   double sigma, wa, wn, wa0, wn0, xj, cj, lj, uj, aj;
   int variant, implicit;
@@ -581,7 +581,7 @@ struct EpiXIter {
     const double wj = __dsub_rn(__dmul_rn(2.0, xb), xj);
     const double xn =
         variant == 0 ? xb : __dadd_rn(__dmul_rn(wa, aj), __dmul_rn(wn, variant == 2 ? wj : xb));
-    if (ef) {
+    if (ef & 2) {
       st_ef(w + j, wj, pol);
       if (x_store || variant != 2) st_ef(x + j, xn, pol);
     } else {

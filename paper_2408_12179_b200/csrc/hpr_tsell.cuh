@@ -82,6 +82,12 @@ __global__ void k_ts_plan(const int *slice_ptr, int s_lo, int s_hi, long long T,
   blk[b] = a;
 }
 
+#ifndef HPR_TS_REV
+#define HPR_TS_REV 0         // 1: each CTA walks its blocks last to first (C3: 836.3 vs 833.1 us, off)
+#endif
+// the i-th block a CTA processes, as an index into its round-robin share
+__device__ __forceinline__ int ts_bi(int i, int nmine) { return HPR_TS_REV ? nmine - 1 - i : i; }
+
 template <int U, class Epi>
 __global__ void __launch_bounds__(kTsThreads, kTsCps)
 k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict__ blk, int nblk) {
@@ -109,7 +115,7 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
       // 32 blocks' slice ranges at once (one lane each), handed to lane 0
       int sb = 0, se = 0, pa = 0, pz = 0;
       if (i0 + lane < nmine) {
-        const int b = g + (i0 + lane) * G;
+        const int b = g + ts_bi(i0 + lane, nmine) * G;
         sb = blk[b];
         se = blk[b + 1];
         pa = M.slice_ptr[sb];
@@ -150,16 +156,16 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
   asm volatile("griddepcontrol.wait;" ::: "memory");
   int nb_s = 0, nb_e = 0;
   if (nmine > 0) {
-    nb_s = blk[g];
-    nb_e = blk[g + 1];
+    nb_s = blk[g + ts_bi(0, nmine) * G];
+    nb_e = blk[g + ts_bi(0, nmine) * G + 1];
   }
   int rot = 0;   // slices of the CTA's earlier blocks: the warp rotation continues across blocks
   for (int i = 0; i < nmine; ++i) {
     const int st = i % kTsStages;
     const int s_b = nb_s, s_e = nb_e;
     if (i + 1 < nmine) {   // next block's slice range, loaded one block ahead
-      nb_s = blk[g + (i + 1) * G];
-      nb_e = blk[g + (i + 1) * G + 1];
+      nb_s = blk[g + ts_bi(i + 1, nmine) * G];
+      nb_e = blk[g + ts_bi(i + 1, nmine) * G + 1];
     }
     const unsigned char *S = ts_sm + (size_t)st * kTsStageBytes;
     const double *rv = (const double *)S;
