@@ -1265,6 +1265,35 @@ int launch_small(hpr_ctx *c, int G, const SellMat &AT, const SellMat &A, const E
   return HPR_OK;
 }
 
+template <bool GAX, bool GAY>
+int launch_small_power(hpr_ctx *c, int G, const SellMat &AT, const SellMat &A, double *v,
+                       double *u, double *wv, double *part) {
+  auto kern = k_small_power<GAX, GAY>;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int &o = g_attr[{(const void *)kern, c->device}];
+    if (o == 0) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      o = 1;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, AT, A, v, u, wv, part, c->pow, (int)c->d.m));
+  CKL();
+  c->launches += 1;
+  return HPR_OK;
+}
+
 int run_small(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, double lamsig,
               int variant) {
   const hpr_buffers &B = c->B;
@@ -1732,6 +1761,22 @@ int hpr_power(hpr_ctx *c, double tol, int max_iters, hpr_power_out *out) {
     out->raw = 0.0;
     out->iterations = 0;
     out->converged = 0;
+    return HPR_OK;
+  }
+  if (const int G = small_cluster(c)) {
+    // small LP: every step in one resident cluster launch (hpr_small.cuh)
+    const SellMat A = c->mat_a(true), AT = c->mat_at(true);
+    rc = AT.ga ? (A.ga ? launch_small_power<true, true>(c, G, AT, A, v, u, wv, P.powa)
+                       : launch_small_power<true, false>(c, G, AT, A, v, u, wv, P.powa))
+               : (A.ga ? launch_small_power<false, true>(c, G, AT, A, v, u, wv, P.powa)
+                       : launch_small_power<false, false>(c, G, AT, A, v, u, wv, P.powa));
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->h_pow, c->pow, sizeof(PowState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out->raw = c->h_pow->lam;
+    out->value = c->h_pow->lam * (1.0 + 1e-3);
+    out->iterations = c->h_pow->iters;
+    out->converged = c->h_pow->converged;
     return HPR_OK;
   }
   if (!c->pow_graph) {

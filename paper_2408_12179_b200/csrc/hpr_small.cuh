@@ -66,4 +66,54 @@ k_small_inner(SellMat AT, SellMat A, const double *y, const double *w, EpiXIter 
   }
 }
 
+// The power method (sparse.py:184-198) for the same small LPs: one cluster
+// launch runs every step -- u = A^T v, w = A u with the per-CTA partials of
+// v.w and ||w||^2, the fixed-order step on CTA 0 (pow_step_block, as the graph
+// path's last CTA), v = w / ||w|| -- with cluster barriers between the
+// phases, until PowState.done.  The state and the vectors other CTAs write
+// are read with coherent loads after the barriers' acquire.
+__device__ __forceinline__ int pow_done(const PowState *S) {
+  return *(volatile const int *)&S->done;
+}
+
+template <bool GAX, bool GAY>
+__global__ void __launch_bounds__(kThreads)
+k_small_power(SellMat AT, SellMat A, double *v, double *u, double *wv, double *part, PowState *S,
+              int m) {
+  const uint64_t pol = policy_evict_last();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  EpiPowTu eu{};
+  eu.u = u;
+  eu.S = S;
+  EpiPowA ea{};
+  ea.v = v;
+  ea.wv = wv;
+  ea.S = S;
+  while (!pow_done(S)) {
+    small_phase<GAX>(AT, v, eu, pol);                 // u = A^T v
+    cluster_barrier();
+    double acc[2] = {0.0, 0.0};                       // w = A u, partials of v.w, ||w||^2
+    {
+      const int nwin = (A.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+      for (int win = blockIdx.x; win < nwin; win += G) {
+        const SliceHdr h = load_hdr(A, win * kWarpsPerCta + wib, lane);
+        sell_slice<GAY ? 4 : HPR_SELL_U, GAY, EpiPowA, true>(A, h, lane, u, ea, acc, pol);
+      }
+      for (int li = blockIdx.x * kWarpsPerCta + wib; li < A.nlong; li += G * kWarpsPerCta)
+        long_row<EpiPowA, true>(A, A.long_rows[li], lane, u, ea, acc, pol);
+    }
+    block_reduce_store<2>(acc, part, G);
+    cluster_barrier();
+    if (blockIdx.x == 0) pow_step_block(part, G, S);  // lambda, ||w||, convergence
+    cluster_barrier();
+    if (*(volatile const int *)&S->norm_pending) {    // v = w / ||w||
+      const double nw = *(volatile const double *)&S->nw;
+      for (int i = blockIdx.x * kThreads + threadIdx.x; i < m; i += G * kThreads)
+        v[i] = __ddiv_rn(ld_coherent(wv + i), nw);
+    }
+    cluster_barrier();
+  }
+}
+
 }  // namespace hpr
