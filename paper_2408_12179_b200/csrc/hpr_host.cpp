@@ -42,8 +42,19 @@ struct Lp {
   int64_t nt = 0, nb = 0, mt = 0, mb = 0, n = 0;
 };
 
+// every array whose buffer is read after the GIL is released stays referenced
+// here (an attribute may be a property that builds a fresh array)
+thread_local std::vector<py::object> *g_keep = nullptr;
+
+py::array as_array(const py::handle &o) {   // an ndarray, or a conversion of a sequence
+  py::array a = py::array::ensure(o);
+  if (!a) throw std::invalid_argument("expected an array");
+  if (g_keep) g_keep->push_back(a);
+  return a;
+}
+
 Idx idx_of(const py::handle &o) {
-  py::array a = py::reinterpret_borrow<py::array>(o);
+  py::array a = as_array(o);
   if (!(a.flags() & py::array::c_style)) throw std::invalid_argument("index array not contiguous");
   Idx r;
   r.p = a.data();
@@ -55,7 +66,7 @@ Idx idx_of(const py::handle &o) {
 }
 
 const double *f64_of(const py::handle &o, int64_t need) {
-  py::array a = py::reinterpret_borrow<py::array>(o);
+  py::array a = as_array(o);
   if (!a.dtype().is(py::dtype::of<double>()) || !(a.flags() & py::array::c_style))
     throw std::invalid_argument("value arrays must be contiguous float64");
   if (a.size() < need) throw std::invalid_argument("value array too short");
@@ -79,6 +90,12 @@ void pack_batch(py::sequence problems, py::dict out, py::array_t<int64_t> row_of
   const int64_t cnt = (int64_t)py::len(problems);
   const int64_t *ro = row_off.data(), *co = col_off.data(), *zo = nz_off.data();
   std::vector<Lp> lps(cnt);
+  std::vector<py::object> keep;
+  keep.reserve((size_t)cnt * 11);
+  struct KeepScope {
+    explicit KeepScope(std::vector<py::object> *k) { g_keep = k; }
+    ~KeepScope() { g_keep = nullptr; }
+  } keep_scope(&keep);
   for (int64_t i = 0; i < cnt; ++i) {     // GIL held: attribute reads only
     py::handle p = problems[i];
     py::object at = p.attr("a_eq"), ab = p.attr("a_ineq");
