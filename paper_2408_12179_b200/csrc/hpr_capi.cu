@@ -401,6 +401,9 @@ struct hpr_ctx {
   long long ts_T[2] = {0, 0};          // block weight targets (0: TS off for A / A^T)
   long long ts_cap_n[2] = {0, 0};      // reserved list entries
   int ts_nb_a = 0, ts_nb_at = 0;
+  // small-LP loop staging (small_smem_plan): cluster size it was planned for,
+  // per-CTA slot capacity of A^T / A, dynamic shared-memory bytes
+  int small_G = -1, small_cap[2] = {0, 0}, small_smem = 0;
   bool ts_a = false, ts_at = false;
   // row-block column chunks of A^T (slices per chunk, 0: one range): the A^T
   // plan is then cut per chunk, chunk q = blocks [ts_at_off[q], ts_at_off[q+1])
@@ -1236,10 +1239,65 @@ int small_cluster(hpr_ctx *c) {
   return G;
 }
 
+// Shared-memory staging of the small loop (k_small_inner): per CTA the largest
+// owned slot count of A^T / A and the bytes of both stages; 0 when the stages
+// exceed the budget or HPR_SMALL_SMEM=0 (the loop then streams from L2).
+size_t small_stage_bytes(int nsl, int cap) {
+  return 4 * (size_t)((nsl + 4) & ~3) + 4 * (size_t)nsl * kSlice +
+         2 * (size_t)((nsl * kSlice + 7) & ~7) + 16 + 12 * (size_t)cap + 16;
+}
+int small_smem_plan(hpr_ctx *c, int G) {
+  if (c->small_G == G) return HPR_OK;
+  c->small_G = G;
+  c->small_cap[0] = c->small_cap[1] = 0;
+  c->small_smem = 0;
+  const char *env = getenv("HPR_SMALL_SMEM");
+  if (env && env[0] == '0') return HPR_OK;
+  int caps[2] = {0, 0};
+  size_t bytes[2] = {0, 0};
+  const Sell *SS[2] = {&c->sat, &c->sa};
+  for (int q = 0; q < 2; ++q) {
+    const Sell &S = *SS[q];
+    std::vector<int> sp(S.nslices + 1);
+    CK(cudaMemcpyAsync(sp.data(), S.slice_ptr, sizeof(int) * (S.nslices + 1),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int nwin = (S.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int nown = (nwin + G - 1) / G;
+    for (int g = 0; g < G; ++g) {
+      long long slots = 0;
+      for (int win = g; win < nwin; win += G)
+        for (int w = 0; w < kWarpsPerCta; ++w) {
+          const int sl = win * kWarpsPerCta + w;
+          if (sl < S.nslices) slots += sp[sl + 1] - sp[sl];
+        }
+      caps[q] = (int)std::max<long long>(caps[q], slots);
+    }
+    bytes[q] = small_stage_bytes(nown * kWarpsPerCta, std::max(caps[q], 1)) + 16;
+  }
+  // within the default 48 KB (more dynamic shared memory cut B200's maximum
+  // cluster size for this kernel from 16 to 8): A first (longer rows, more
+  // dependent batches per slice), then A^T if it fits too
+  constexpr size_t kBudget = 48 * 1024;
+  size_t total = 0;
+  if (bytes[1] <= kBudget) {
+    c->small_cap[1] = std::max(caps[1], 1);
+    total += bytes[1];
+  }
+  if (total + bytes[0] <= kBudget) {
+    c->small_cap[0] = std::max(caps[0], 1);
+    total += bytes[0];
+  }
+  c->small_smem = (int)total;
+  return HPR_OK;
+}
+
 template <bool GAX, bool GAY>
 int launch_small(hpr_ctx *c, int G, const SellMat &AT, const SellMat &A, const EpiXIter &ex,
                  const EpiYIter &ey, int steps) {
   auto kern = k_small_inner<GAX, GAY>;
+  if (int e = small_smem_plan(c, G)) return e;
+
   {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int &o = g_attr[{(const void *)kern, c->device}];
@@ -1259,8 +1317,9 @@ int launch_small(hpr_ctx *c, int G, const SellMat &AT, const SellMat &A, const E
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  cfg.dynamicSmemBytes = c->small_smem;
   CK(cudaLaunchKernelEx(&cfg, kern, AT, A, (const double *)c->B.y, (const double *)c->B.w, ex, ey,
-                        steps, (int)HPR_X_IMPLICIT));
+                        steps, (int)HPR_X_IMPLICIT, c->small_cap[0], c->small_cap[1]));
   CKL();
   return HPR_OK;
 }
@@ -1576,6 +1635,7 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   }
   rc = ts_plan(c);
   if (rc) return rc;
+  c->small_G = -1;   // the small loop's staging plan follows the layout
   c->laid_out = true;
   c->scaled = false;
   return HPR_OK;

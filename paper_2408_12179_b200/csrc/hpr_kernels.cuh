@@ -285,7 +285,15 @@ template <class E>
 struct has_final<E, std::void_t<decltype(std::declval<E &>().final(nullptr, 0))>>
     : std::true_type {};
 
-template <int U, bool GA, class Epi, bool COH = false>
+// matrix-stream load: global (streaming, L2 hint) or, SM = true, a copy of the
+// slices in shared memory (the resident small-LP loop)
+template <bool SM, class T>
+__device__ __forceinline__ T ld_mat(const T *ptr, uint64_t pol) {
+  if constexpr (SM) return *ptr;
+  else return ld_stream(ptr, pol);
+}
+
+template <int U, bool GA, class Epi, bool COH = false, bool SM = false>
 __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, int lane,
                                            const double *__restrict__ xg, Epi &epi, double *acc,
                                            uint64_t pol) {
@@ -305,8 +313,8 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (u < len) {
-      c[u] = ld_stream(cp + u * kSlice, pol);
-      v[u] = ld_stream(vp + u * kSlice, pol);
+      c[u] = ld_mat<SM>(cp + u * kSlice, pol);
+      v[u] = ld_mat<SM>(vp + u * kSlice, pol);
     }
   if constexpr (GA && HPR_GA_LEAN) {
   // lean depth-2 pipeline: batch k+1's gathers and batch k+2's column
@@ -319,7 +327,7 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
   int c1[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (U + u < len) c1[u] = ld_stream(cp + (U + u) * kSlice, pol);
+    if (U + u < len) c1[u] = ld_mat<SM>(cp + (U + u) * kSlice, pol);
   for (int k = 0; k < slen; k += U) {
     double x1[U], v1[U];
     int c2[U];
@@ -327,11 +335,11 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
     for (int u = 0; u < U; ++u)
       if (k + U + u < len) {
         x1[u] = gather<COH>(xg + c1[u]);
-        v1[u] = ld_stream(vp + (k + U + u) * kSlice, pol);
+        v1[u] = ld_mat<SM>(vp + (k + U + u) * kSlice, pol);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (k + 2 * U + u < len) c2[u] = ld_stream(cp + (k + 2 * U + u) * kSlice, pol);
+      if (k + 2 * U + u < len) c2[u] = ld_mat<SM>(cp + (k + 2 * U + u) * kSlice, pol);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], x0[u]));
@@ -355,8 +363,8 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (U + u < len) {
-      c1[u] = ld_stream(cp + (U + u) * kSlice, pol);
-      v1[u] = ld_stream(vp + (U + u) * kSlice, pol);
+      c1[u] = ld_mat<SM>(cp + (U + u) * kSlice, pol);
+      v1[u] = ld_mat<SM>(vp + (U + u) * kSlice, pol);
     }
   for (int k = 0; k < slen; k += U) {
     double x1[U];
@@ -368,8 +376,8 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + 2 * U + u < len) {
-        c2[u] = ld_stream(cp + (k + 2 * U + u) * kSlice, pol);
-        v2[u] = ld_stream(vp + (k + 2 * U + u) * kSlice, pol);
+        c2[u] = ld_mat<SM>(cp + (k + 2 * U + u) * kSlice, pol);
+        v2[u] = ld_mat<SM>(vp + (k + 2 * U + u) * kSlice, pol);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -389,8 +397,8 @@ __device__ __forceinline__ void sell_slice(const SellMat &M, const SliceHdr &h, 
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + U + u < len) {
-        cn[u] = ld_stream(cp + (k + U + u) * kSlice, pol);
-        vn[u] = ld_stream(vp + (k + U + u) * kSlice, pol);
+        cn[u] = ld_mat<SM>(cp + (k + U + u) * kSlice, pol);
+        vn[u] = ld_mat<SM>(vp + (k + U + u) * kSlice, pol);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)

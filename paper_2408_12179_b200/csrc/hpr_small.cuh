@@ -44,24 +44,117 @@ __device__ __forceinline__ void small_phase(const SellMat &M, const double *xg, 
     long_row<Epi, true>(M, M.long_rows[li], lane, xg, epi, acc, pol);
 }
 
+// Shared-memory residency of a CTA's slices (HPR_SMALL_SMEM): the CTA's
+// windows of one matrix (win = blockIdx.x + q G), slice by slice, each slice's
+// slots in their SELL order; per owned slice (q, warp) its shared-memory slot
+// base and, for a non-compact slice, the lanes' rows / lengths.  Loaded once
+// per interval launch, read every iteration (the matrix streams no longer go
+// to L2).
+struct SmallStage {
+  int *base;            // [kSmallMaxOwn * kWarpsPerCta]
+  int *row;             // [kSmallMaxOwn * kWarpsPerCta * 32]
+  unsigned short *len;  // same
+  int *ci;
+  double *val;
+};
+constexpr int kSmallMaxOwn = kSmallMaxWin / 1;   // windows per CTA (G >= 1)
+
+__device__ __forceinline__ int small_stage(const SellMat &M, SmallStage &S, unsigned char *p,
+                                           int cap_slots) {
+  const int G = gridDim.x, tid = threadIdx.x;
+  const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int nown = blockIdx.x < nwin ? (nwin - blockIdx.x + G - 1) / G : 0;
+  const int nsl = nown * kWarpsPerCta;
+  S.base = (int *)p;
+  S.row = S.base + ((nsl + 4) & ~3);
+  S.len = (unsigned short *)(S.row + nsl * kSlice);
+  unsigned char *q = (unsigned char *)(S.len + ((nsl * kSlice + 7) & ~7));
+  S.val = (double *)(((uintptr_t)q + 15) & ~(uintptr_t)15);
+  S.ci = (int *)(S.val + cap_slots);
+  // slot bases (thread 0 scans the owned slices' sizes in order)
+  if (tid == 0) {
+    int o = 0;
+    for (int k = 0; k < nsl; ++k) {
+      const int s = (blockIdx.x + (k / kWarpsPerCta) * G) * kWarpsPerCta + k % kWarpsPerCta;
+      S.base[k] = o;
+      if (s < M.nslices) o += M.slice_ptr[s + 1] - M.slice_ptr[s];
+    }
+    S.base[nsl] = o;
+  }
+  __syncthreads();
+  for (int k = 0; k < nsl; ++k) {
+    const int s = (blockIdx.x + (k / kWarpsPerCta) * G) * kWarpsPerCta + k % kWarpsPerCta;
+    if (s >= M.nslices) break;
+    const int a = M.slice_ptr[s], n = M.slice_ptr[s + 1] - a, b = S.base[k];
+    for (int t = tid; t < n; t += kThreads) {
+      S.val[b + t] = M.val[a + t];
+      S.ci[b + t] = M.ci[a + t];
+    }
+    if (tid < kSlice) {
+      const SliceHdr h = load_hdr(M, s, tid);
+      S.row[k * kSlice + tid] = h.row;
+      S.len[k * kSlice + tid] = (unsigned short)h.len;
+    }
+  }
+  __syncthreads();
+  return nsl;
+}
+
+template <bool GA, class Epi>
+__device__ __forceinline__ void small_phase_sm(const SellMat &M, const SmallStage &S,
+                                               const double *xg, Epi &epi, uint64_t pol) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  const int nwin = (M.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
+  double acc[1] = {0.0};
+  SellMat Ms = M;
+  Ms.ci = S.ci;
+  Ms.val = S.val;
+  for (int win = blockIdx.x, q = 0; win < nwin; win += G, ++q) {
+    const int k = q * kWarpsPerCta + wib, s = win * kWarpsPerCta + wib;
+    SliceHdr h{-1, 0, 0, 0};
+    if (s < M.nslices) {
+      h.row = S.row[k * kSlice + lane];
+      h.len = S.len[k * kSlice + lane];
+      h.base = S.base[k];
+      h.slen = (S.base[k + 1] - S.base[k]) / kSlice;
+    }
+    sell_slice<GA ? 4 : HPR_SELL_U, GA, Epi, true, true>(Ms, h, lane, xg, epi, acc, pol);
+  }
+  for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += G * kWarpsPerCta)
+    long_row<Epi, true>(M, M.long_rows[li], lane, xg, epi, acc, pol);
+}
+
 // `steps` HPR iterations: x-phase over A^T (gathers y), barrier, y-phase over
 // A (gathers w), barrier.  x_implicit: HPR keeps x implicit between the first
-// and last step (EpiXIter).
+// and last step (EpiXIter).  cap_a / cap_at > 0: the CTA's slices of A / A^T
+// are staged in shared memory (capacity in slots; A first, then A^T).
 template <bool GAX, bool GAY>
 __global__ void __launch_bounds__(kThreads)
 k_small_inner(SellMat AT, SellMat A, const double *y, const double *w, EpiXIter ex, EpiYIter ey,
-              int steps, int x_implicit) {
+              int steps, int x_implicit, int cap_at, int cap_a) {
+  extern __shared__ __align__(16) unsigned char small_sm[];
   const uint64_t pol = policy_evict_last();      // the whole LP stays in L2
+  SmallStage SAT{}, SA{};
+  const bool sm_at = cap_at > 0, sm_a = cap_a > 0;
+  unsigned char *p = small_sm;
+  if (sm_a) {
+    small_stage(A, SA, p, cap_a);
+    p = (unsigned char *)(((uintptr_t)(SA.ci + cap_a) + 15) & ~(uintptr_t)15);
+  }
+  if (sm_at) small_stage(AT, SAT, p, cap_at);
   for (int i = 0; i < steps; ++i) {
     ex.step = i;
     ex.x_from_w = x_implicit && i > 0;
     ex.x_store = !x_implicit || i == steps - 1;
     ex.enter();
-    small_phase<GAX>(AT, y, ex, pol);
+    if (sm_at) small_phase_sm<GAX>(AT, SAT, y, ex, pol);
+    else small_phase<GAX>(AT, y, ex, pol);
     cluster_barrier();
     ey.step = i;
     ey.enter();
-    small_phase<GAY>(A, w, ey, pol);
+    if (sm_a) small_phase_sm<GAY>(A, SA, w, ey, pol);
+    else small_phase<GAY>(A, w, ey, pol);
     cluster_barrier();
   }
 }

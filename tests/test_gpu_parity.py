@@ -523,10 +523,13 @@ def test_flow_lp_compact_many_blocks_bit_exact(ts, monkeypatch):
     dev.close()
 
 
-def test_small_resident_loop_matches_graph_path(monkeypatch):
+@pytest.mark.parametrize("smem", ["1", "0"])
+def test_small_resident_loop_matches_graph_path(smem, monkeypatch):
     """The resident small-LP loop (one cluster launch per interval, default for
-    C1-size LPs) and the per-iteration graph path give the same solve: same
+    C1-size LPs; slices staged in shared memory or, HPR_SMALL_SMEM=0, streamed
+    from L2) and the per-iteration graph path give the same solve: same
     report, bit-identical solution."""
+    monkeypatch.setenv("HPR_SMALL_SMEM", smem)
     prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
     cfg = P.SolverConfig(tolerance=1e-8)
     reps = {}
