@@ -85,6 +85,41 @@ def load_traffic(config):
     return None
 
 
+def phase_bytes(m, n, nnz, bu=0):
+    """Algorithmic bytes of the x-phase and the y-phase as hpr_time_phases
+    runs them (an interval's steady-state HPR step): the matrix (12 B per
+    entry) and its row pointers, the gathered vector once, the streamed row
+    operands and the writes -- x re-formed from w and not stored, uniform
+    bounds (bu bits) passed as scalars."""
+    streams_x = 5 - (bu & 1) - ((bu >> 1) & 1)          # w (for x), c, l, u, anchor
+    bx = 12 * nnz + 4 * (n + 1) + 8 * m + 8 * streams_x * n + 8 * 1 * n
+    by = 12 * nnz + 4 * (m + 1) + 8 * n + 8 * 3 * m + 8 * m
+    return bx, by
+
+
+def phase_roofline(m, n, nnz, lay, x_us, y_us, peak):
+    """Per-kernel HBM roofline of the two iteration kernels, each timed alone
+    (20 back-to-back launches, CUDA events; hpr_time_phases), and the random
+    operand-gather rate of each (one 8-byte gather per entry)."""
+    if x_us is None:
+        return None
+    bx, by = phase_bytes(m, n, nnz, int(lay.get("bounds_uniform", 0)))
+    kx, ky = iteration_kernels(lay).split(" (")[0].split(" + ")
+    gpeak = gather_peak()
+    out = {}
+    for name, k, b, us in (("x_phase", kx, bx, x_us), ("y_phase", ky, by, y_us)):
+        gbs = b / (us * 1e-6) / 1e9
+        out[name] = {"kernel": k, "us_per_launch": us, "bytes": b, "achieved_gbs": gbs,
+                     "frac": gbs / peak, "gathers_per_s": nnz / (us * 1e-6),
+                     "gather_frac": nnz / (us * 1e-6) / gpeak}
+    out["note"] = ("each kernel alone, 20 back-to-back launches of an interval's steady-state "
+                   "step after the timed region; bytes = the phase's algorithmic bytes (x "
+                   "implicit, uniform bounds as scalars); gather_frac = random operand "
+                   "gathers against one L1TEX wavefront per cycle per SM (a staged phase "
+                   "gathers from shared memory)")
+    return out
+
+
 def iteration_kernels(lay):
     """Names of the two iteration kernels the layout selected."""
     x = ("k_stg<EpiXIter>" if lay.get("stg_at") else
@@ -100,16 +135,20 @@ def iteration_kernels(lay):
     return f"{x} + {y} (one HPR iteration)"
 
 
+def gather_peak():
+    """One L1TEX wavefront per cycle per SM at the max SM clock (gathers/s)."""
+    import torch
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    mhz = float(json.load(open(p)).get("sm_max_mhz", 1965.0)) if os.path.exists(p) else 1965.0
+    return torch.cuda.get_device_properties(0).multi_processor_count * mhz * 1e6
+
+
 def gather_roofline(nnz, iterations, seconds, lay=None):
     """Operand gathers per second against one L1TEX wavefront per cycle per SM
     (148 SMs at the max SM clock): nnz gathers per HPR iteration for each phase
     on the SELL engine (a staged phase gathers from shared memory); None when
     both phases are staged."""
-    import torch
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    mhz = float(json.load(open(p)).get("sm_max_mhz", 1965.0)) if os.path.exists(p) else 1965.0
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
-    peak = sms * mhz * 1e6
+    peak = gather_peak()
     lay = lay or {}
     sell_phases = int(not lay.get("stg_at")) + int(not lay.get("stg_a"))
     if sell_phases == 0:
@@ -588,6 +627,10 @@ def run_ours(args):
     launches = dev.launch_count() - l0
     t_max, its_all = _max_sum(dist, local, total_ms / 1e3, its_total)
     value = its_all / t_max
+    # the two iteration kernels one at a time (after the timed region: the
+    # diagnostic overwrites the iterate), for the per-kernel roofline
+    lay_now = dev.layout_info()
+    ph_x_us, ph_y_us = (None, None) if dev.small_path() else dev.time_phases(20)
 
     # e2e through the public API from host arrays: every step uploads the
     # problem (pinned staging -> H2D), re-analyses it, solves and copies the
@@ -650,6 +693,7 @@ def run_ours(args):
                          "frac_required": b_req * its_total / iter_s_total / 1e9 / peak,
                          "timing": "CUDA events on the solver stream around each "
                                    "150-iteration graph replay (the two iteration kernels)"},
+            "roofline_phases": phase_roofline(m, n, nnz, lay_now, ph_x_us, ph_y_us, peak),
             # the bound that actually binds a small-n problem (C2): every nonzero
             # is one random 8-byte operand gather = one L1TEX wavefront per cycle per SM
             # (phases on the staged engine gather from shared memory instead)

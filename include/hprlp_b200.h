@@ -248,6 +248,16 @@ int hpr_trsolve(int m, const double *linv, const double *linv_t, const double *r
 /* Device time (ms) of the last hpr_run_inner and of the last checkpoint,
  * measured with CUDA events on the context stream. */
 int hpr_last_times(hpr_ctx *ctx, double *inner_ms, double *ckpt_ms);
+/* Diagnostic (bench.py): `reps` back-to-back launches of the x-phase kernel
+   (an interval's steady-state step: for HPR, x re-formed from w and not
+   stored), then of the y-phase kernel, on the engines the layout selected; average
+   microseconds per launch from CUDA events on the context's stream.  Runs
+   iterations on the current state (the iterate is overwritten): call it after
+   a solve, never inside one. */
+int hpr_time_phases(hpr_ctx *ctx, int reps, double *x_us, double *y_us);
+/* 1 when hpr_run_inner runs the resident small-LP loop (one cluster launch
+   per interval, hpr_small.cuh) for this context's layout, else 0. */
+int hpr_small_path(hpr_ctx *ctx);
 
 /* ------------------------------------------------------------------------
  * Row-block partitioned mode (paper_2408_12179_b200/csrc/

@@ -150,6 +150,10 @@ _SIGS = {
     "hpr_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "hpr_layout_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(HprLayoutInfo)]),
     "hpr_spmv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "hpr_small_path": (ctypes.c_int, [ctypes.c_void_p]),
+    "hpr_time_phases": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double)]),
     "hpr_last_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                       ctypes.POINTER(ctypes.c_double)]),
     # exact T1 = 0 path (hpr_exact.cuh)

@@ -1934,6 +1934,46 @@ int l2_window_setup(hpr_ctx *c) {
   return HPR_OK;
 }
 
+// the inner-loop epilogues of the graph path (step fields set per launch)
+static void iter_epilogues(const hpr_ctx *c, EpiXIter &ex, EpiYIter &ey) {
+  const hpr_buffers &B = c->B;
+  ex = EpiXIter{};
+  ex.c = B.c_s;
+  ex.lo = B.lower_s;
+  ex.up = B.upper_s;
+  ex.bounds_uniform = c->bounds_uniform;
+  ex.lo_u = c->lo_u;
+  ex.up_u = c->up_u;
+  ex.anc = B.anc_x;
+  ex.x = B.x;
+  ex.w = B.w;
+  ex.P = c->params;
+  ey = EpiYIter{};
+  ey.b = B.b_s;
+  ey.anc = B.anc_y;
+  ey.y = B.y;
+  ey.P = c->params;
+  ey.m1 = (int)c->d.m1;
+  ey.ef = HPR_Y_EF && c->ts_at;   // with the TS x-phase (HBM-bound problems)
+}
+
+// one x-phase / y-phase launch on the engine the layout selected
+static int launch_x_phase(hpr_ctx *c, const EpiXIter &ex, bool pdl) {
+  const hpr_buffers &B = c->B;
+  return c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
+         : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
+         : c->ts_at ? launch_ts(c, c->mat_at(true), c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, B.y,
+                                ts_ef(ex))
+                    : launch_sell(c, c->mat_at(true), B.y, ex, nullptr, nullptr, pdl);
+}
+static int launch_y_phase(hpr_ctx *c, const EpiYIter &ey) {
+  const hpr_buffers &B = c->B;
+  return c->sta.on ? launch_stg(c, c->sta, (int)c->d.n, B.w, ey)
+         : c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
+         : c->ts_a ? launch_ts(c, c->mat_a(true), c->ts_blk, c->ts_nb_a, B.w, ey)
+                   : launch_a_iter(c, B.w, ey, true);
+}
+
 int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, double lamsig,
                   int variant) {
   int rc = check_ctx(c, true, true);
@@ -1948,23 +1988,8 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
   if (it == c->inner_graphs.end()) {
     const SellMat A = c->mat_a(true), AT = c->mat_at(true);
     EpiXIter ex{};
-    ex.c = B.c_s;
-    ex.lo = B.lower_s;
-    ex.up = B.upper_s;
-    ex.bounds_uniform = c->bounds_uniform;
-    ex.lo_u = c->lo_u;
-    ex.up_u = c->up_u;
-    ex.anc = B.anc_x;
-    ex.x = B.x;
-    ex.w = B.w;
-    ex.P = c->params;
     EpiYIter ey{};
-    ey.b = B.b_s;
-    ey.anc = B.anc_y;
-    ey.y = B.y;
-    ey.P = c->params;
-    ey.m1 = (int)c->d.m1;
-    ey.ef = HPR_Y_EF && c->ts_at;   // with the TS x-phase (HBM-bound problems)
+    iter_epilogues(c, ex, ey);
     cudaGraph_t g;
     const long long before = c->launches;
     if (int e2 = l2_window_setup(c)) return e2;
@@ -1976,15 +2001,8 @@ int hpr_run_inner(hpr_ctx *c, int steps, int64_t t, int64_t k, double sigma, dou
       ex.x_from_w = HPR_X_IMPLICIT && i > 0;
       ex.x_store = !HPR_X_IMPLICIT || i == steps - 1;
       // the first kernel of the graph follows the k_set_params launch: plain edge
-      int rc2 = c->stat.on ? launch_stg(c, c->stat, (int)c->d.m, B.y, ex)
-                : c->cbat.on ? launch_cb(c, c->cbat, (int)c->d.m, B.y, ex)
-                : c->ts_at ? launch_ts(c, AT, c->ts_blk + c->ts_nb_a + 1, c->ts_nb_at, B.y, ts_ef(ex))
-                             : launch_sell(c, AT, B.y, ex, nullptr, nullptr, i > 0);
-      if (!rc2)
-        rc2 = c->sta.on ? launch_stg(c, c->sta, (int)c->d.n, B.w, ey)
-              : c->cba.on ? launch_cb(c, c->cba, (int)c->d.n, B.w, ey)
-              : c->ts_a ? launch_ts(c, A, c->ts_blk, c->ts_nb_a, B.w, ey)
-                          : launch_a_iter(c, B.w, ey, true);
+      int rc2 = launch_x_phase(c, ex, i > 0);
+      if (!rc2) rc2 = launch_y_phase(c, ey);
       if (rc2) {
         c->l2win_active = false;
         cudaStreamEndCapture(s, &g);
@@ -2155,6 +2173,36 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->bounds_uniform = c->bounds_uniform;
   info->ts_a = c->ts_a ? c->ts_nb_a : 0;
   info->ts_at = c->ts_at ? c->ts_nb_at : 0;
+  return HPR_OK;
+}
+
+int hpr_small_path(hpr_ctx *c) { return c && c->analyzed && small_cluster(c) > 0 ? 1 : 0; }
+
+int hpr_time_phases(hpr_ctx *c, int reps, double *x_us, double *y_us) {
+  int rc = check_ctx(c, true, true);
+  if (rc) return rc;
+  if (reps < 1 || !x_us || !y_us) return fail(HPR_EINVAL, "bad argument");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  EpiXIter ex{};
+  EpiYIter ey{};
+  iter_epilogues(c, ex, ey);
+  ex.step = ey.step = 1;
+  ex.x_from_w = HPR_X_IMPLICIT;   // an interval's steady-state step (x implicit for HPR)
+  ex.x_store = !HPR_X_IMPLICIT;
+  CK(cudaEventRecord(c->ev0, s));
+  for (int r = 0; r < reps && !rc; ++r) rc = launch_x_phase(c, ex, false);
+  CK(cudaEventRecord(c->ev1, s));
+  for (int r = 0; r < reps && !rc; ++r) rc = launch_y_phase(c, ey);
+  CK(cudaEventRecord(c->ev2, s));
+  if (rc) return rc;
+  CK(cudaEventSynchronize(c->ev2));
+  float a = 0.f, b = 0.f;
+  CK(cudaEventElapsedTime(&a, c->ev0, c->ev1));
+  CK(cudaEventElapsedTime(&b, c->ev1, c->ev2));
+  *x_us = 1e3 * a / reps;
+  *y_us = 1e3 * b / reps;
+  c->inner_timed = c->ckpt_timed = false;   // the events now hold this measurement
   return HPR_OK;
 }
 

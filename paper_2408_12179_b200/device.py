@@ -317,6 +317,18 @@ class DeviceLP:
         N.call("hpr_layout_info", self.ctx, ctypes.byref(info))
         return {f: int(getattr(info, f)) for f, _ in N.HprLayoutInfo._fields_}
 
+    def small_path(self) -> bool:
+        """True when run_inner takes the resident small-LP loop (no separate
+        phase kernels to time)."""
+        return bool(N.load_library().hpr_small_path(self.ctx))
+
+    def time_phases(self, reps: int = 20):
+        """(x-phase, y-phase) microseconds per launch, ``reps`` launches each
+        (hpr_time_phases: overwrites the iterate -- after a solve only)."""
+        a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        N.call("hpr_time_phases", self.ctx, int(reps), ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
     def last_times(self):
         a, b = ctypes.c_double(0), ctypes.c_double(0)
         N.call("hpr_last_times", self.ctx, ctypes.byref(a), ctypes.byref(b))
