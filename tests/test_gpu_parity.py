@@ -543,3 +543,22 @@ def test_small_resident_loop_matches_graph_path(smem, monkeypatch):
         assert np.array_equal(getattr(a.solution, f), getattr(b.solution, f))
     # one launch per interval instead of 2 x check_interval
     assert b.device_stats["launches"] < a.device_stats["launches"]
+
+
+def test_time_phases_diagnostic(monkeypatch):
+    """hpr_time_phases (bench.py's per-kernel roofline): both iteration kernels
+    time positive; the small-LP path is reported as such."""
+    prob, _ = P.generate_known_solution_lp(1, 500, 500, 2000, 0.01)
+    monkeypatch.setenv("HPR_SMALL", "1")
+    dev = _dev(prob)
+    assert dev.small_path()
+    dev.close()
+    monkeypatch.setenv("HPR_SMALL", "0")
+    dev = _dev(prob)
+    assert not dev.small_path()
+    lam = dev.power(1e-4, 5000).raw * 1.001
+    dev.state_reset()
+    dev.run_inner(3, 0, 0, 1.0, lam, 2)
+    x_us, y_us = dev.time_phases(5)
+    assert x_us > 0.0 and y_us > 0.0
+    dev.close()
