@@ -387,7 +387,7 @@ def _build_reports(pk: PackedBatch, raw, lraw, x, y, z, max_log: int = MAX_LOG) 
     return out
 
 
-PIPE_CHUNK = 512       # LPs per pipelined launch (C5 sweep: 4096 / 2048 / 1024 / 512 / 256 -> 217 / 157 / 140 / 133 / 137 ms per call)
+PIPE_CHUNK = 1024      # LPs per pipelined launch (C5, native packing: 4096 / 2048 / 1024 / 512 / 256 -> 161-196 / 124-131 / 122-128 / 122-181 / 129-132 ms per call)
 PIPE_MIN = 2048        # batches smaller than this run as one launch
 
 
