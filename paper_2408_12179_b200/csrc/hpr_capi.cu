@@ -64,6 +64,9 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_SELL_U
 #define HPR_SELL_U 4    // entries per lane per batch without gather-ahead (2 / 8: C3 +20 % / +100 %)
 #endif
+#ifndef HPR_GA_U
+#define HPR_GA_U 3      // entries per lane per batch on the gather-ahead path (4: 80 registers + spills; 3: C2 48.2 -> 46.3 us, C4 rank 1625 -> 1590 us per iteration)
+#endif
 #ifndef HPR_GA_MIN
 #define HPR_GA_MIN 12   // avg row length from which the SELL lanes gather one batch ahead
 #endif                  // (measured: C2 (25/50 per row) -5 %, C3 (3/8-32 per row) +18 % -> long rows only
@@ -533,7 +536,7 @@ int launch_sell_u(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi
 template <class Epi>
 int launch_sell(hpr_ctx *c, const SellMat &M, const double *xg, const Epi &epi, double *part,
                 int *grid_out, bool pdl = false) {
-  return M.ga ? launch_sell_u<4, true>(c, M, xg, epi, part, grid_out, pdl)
+  return M.ga ? launch_sell_u<HPR_GA_U, true>(c, M, xg, epi, part, grid_out, pdl)
               : launch_sell_u<HPR_SELL_U, false>(c, M, xg, epi, part, grid_out, pdl);
 }
 

@@ -38,7 +38,7 @@ __device__ __forceinline__ void small_phase(const SellMat &M, const double *xg, 
   double acc[1] = {0.0};
   for (int win = blockIdx.x; win < nwin; win += G) {
     const SliceHdr h = load_hdr(M, win * kWarpsPerCta + wib, lane);
-    sell_slice<GA ? 4 : HPR_SELL_U, GA, Epi, true>(M, h, lane, xg, epi, acc, pol);
+    sell_slice<GA ? HPR_GA_U : HPR_SELL_U, GA, Epi, true>(M, h, lane, xg, epi, acc, pol);
   }
   for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += G * kWarpsPerCta)
     long_row<Epi, true>(M, M.long_rows[li], lane, xg, epi, acc, pol);
@@ -119,7 +119,7 @@ __device__ __forceinline__ void small_phase_sm(const SellMat &M, const SmallStag
       h.base = S.base[k];
       h.slen = (S.base[k + 1] - S.base[k]) / kSlice;
     }
-    sell_slice<GA ? 4 : HPR_SELL_U, GA, Epi, true, true>(Ms, h, lane, xg, epi, acc, pol);
+    sell_slice<GA ? HPR_GA_U : HPR_SELL_U, GA, Epi, true, true>(Ms, h, lane, xg, epi, acc, pol);
   }
   for (int li = blockIdx.x * kWarpsPerCta + wib; li < M.nlong; li += G * kWarpsPerCta)
     long_row<Epi, true>(M, M.long_rows[li], lane, xg, epi, acc, pol);
@@ -191,7 +191,7 @@ k_small_power(SellMat AT, SellMat A, double *v, double *u, double *wv, double *p
       const int nwin = (A.nslices + kWarpsPerCta - 1) / kWarpsPerCta;
       for (int win = blockIdx.x; win < nwin; win += G) {
         const SliceHdr h = load_hdr(A, win * kWarpsPerCta + wib, lane);
-        sell_slice<GAY ? 4 : HPR_SELL_U, GAY, EpiPowA, true>(A, h, lane, u, ea, acc, pol);
+        sell_slice<GAY ? HPR_GA_U : HPR_SELL_U, GAY, EpiPowA, true>(A, h, lane, u, ea, acc, pol);
       }
       for (int li = blockIdx.x * kWarpsPerCta + wib; li < A.nlong; li += G * kWarpsPerCta)
         long_row<EpiPowA, true>(A, A.long_rows[li], lane, u, ea, acc, pol);
