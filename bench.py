@@ -255,6 +255,39 @@ def make_instance(name):
     return config_instance(name)
 
 
+L2_NOTE = "256 MB buffer written between timed steps (flush)"
+
+
+def shared_config(config, tol, m, n, nnz):
+    """The `config` object both arms print for C1-C3: the workload only (what
+    each arm's step is, and its results, go in the line's `run` object), so
+    the driver's same-config check compares like with like."""
+    return {"workload": CONFIG_NAMES[config], "tolerance": tol, "m": int(m), "n": int(n),
+            "nnz": int(nnz), "l2": L2_NOTE, "parallelism": "none (one device)"}
+
+
+def c5_config(ws):
+    return {"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8, "lps_total": C5_COUNT,
+            "l2": "inputs re-read from HBM each step (490 MB > L2)",
+            "parallelism": f"batch sharded x{ws}" if ws > 1 else "none (one device)"}
+
+
+def c4_config(ws, rows):
+    return {"workload": CONFIG_NAMES["c4"], "tolerance": 1e-8, "n": C4_N,
+            "rows_per_rank": rows, "nnz_per_rank": rows * C4_PER_ROW,
+            "l2": "working set > L2 (no flush needed)",
+            "parallelism": f"row-block x{ws} (NCCL)"}
+
+
+def host_flush():
+    """The reference arm's counterpart of the GPU arm's L2 flush: write 256 MB
+    between timed steps so every step starts with cold host caches."""
+    import numpy as np
+    buf = np.empty(32 * 1024 * 1024, dtype=np.float64)
+    buf.fill(1.0)
+    return float(buf[-1])
+
+
 def c5_problems(lo, hi):
     from paper_2408_12179_b200.generators import generate_known_solution_lp
     return [generate_known_solution_lp(10_000 + i, 250, 250, 1000, 0.01)[0] for i in range(lo, hi)]
@@ -407,7 +440,7 @@ def run_reference(args):
              "d2h_bytes_per_step": 0}
         line["e2e"] = e
         line["cpu_baseline"] = dict(line["cpu_baseline"], value=line["value"])
-        line["config"]["host"] = host_info()
+        line.setdefault("run", {})["host"] = host_info()
         print(json.dumps(line), flush=True)
 
     if config == "c5":
@@ -431,8 +464,8 @@ def run_reference(args):
         who = "hprlp.solve (baseline/_ref)" if hprlp is not None else "the oracle port"
         emit(dict(base, metric="hpr_lp_iterations_per_sec", value=val, unit="LP-it/s",
                   ms_per_step=1e3 * sum(v[1] for v in vals) / len(vals),
-                  config={"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
-                          "step": f"{cnt} of the 4096 C5 LPs solved to 1e-8 by {who}, "
+                  config=c5_config(ws),
+                  run={"step": f"{cnt} of the 4096 C5 LPs solved to 1e-8 by {who}, "
                                   f"one LP per process, {min(cores, cnt)} processes"},
                   cpu_baseline={"unit": "LP-it/s", "cores": min(cores, cnt), "kind": kind,
                                 "sample": f"{args.steps} x {cnt} whole LP solves"}))
@@ -456,15 +489,15 @@ def run_reference(args):
         # one job iteration = ws rank blocks: the whole-job rate in the same
         # unit as our arm (rank-block iterations per second) is the block rate
         emit(dict(base, value=block_its, unit="rank-it/s", ms_per_step=1e3 * dt / args.steps,
-                  config={"workload": CONFIG_NAMES["c4"], "tolerance": 1e-8,
-                          "rows_per_rank": rows,
-                          "step": "1 HPR iteration over one rank block (oracle port; the "
+                  config=c4_config(ws, rows),
+                  run={"step": "1 HPR iteration over one rank block (oracle port; the "
                                   "reference cannot hold C4)"},
                   cpu_baseline={"unit": "rank-it/s", "cores": threads, "kind": "port",
                                 "sample": f"{args.steps} iterations of one 1.25M-row block"}))
         return
 
     prob, tol = make_instance(config)
+    wcfg = shared_config(config, tol, prob.m, prob.n, prob.a_eq.nnz + prob.a_ineq.nnz)
     if hprlp is not None:
         from hprlp.core import ProblemData, SolverState, Variant as RefVariant, run_inner
         from hprlp.scaling import scale_problem
@@ -478,15 +511,16 @@ def run_reference(args):
                 hprlp.solve(rp, cfg)
             its, dt, wall = 0, 0.0, 0.0
             for _ in range(args.steps):
+                host_flush()
                 t0 = time.perf_counter()
                 rep = hprlp.solve(rp, cfg)
                 wall += time.perf_counter() - t0
                 its += rep.iterations
             val = its / wall
             emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * wall / args.steps,
-                      config={"workload": CONFIG_NAMES[config], "tolerance": tol,
-                              "step": "one full hprlp.solve to tolerance (same unit as ours)",
-                              "status": rep.status.value, "iterations_per_solve": rep.iterations},
+                      config=wcfg,
+                      run={"step": "one full hprlp.solve to tolerance (same unit as ours)",
+                           "status": rep.status.value, "iterations_per_solve": rep.iterations},
                       cpu_baseline={"unit": "it/s", "cores": 1, "kind": "reference",
                                     "sample": f"{args.steps} whole solves"}))
             return
@@ -501,14 +535,16 @@ def run_reference(args):
         s = REF_STEP_ITERS.get(config, 150)
         for _ in range(args.warmup):
             run_inner(state, data, s)
-        t0 = time.perf_counter()
+        dt = 0.0
         for _ in range(args.steps):
+            host_flush()
+            t0 = time.perf_counter()
             run_inner(state, data, s)
-        dt = time.perf_counter() - t0
+            dt += time.perf_counter() - t0
         val = s * args.steps / dt
         emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
-                  config={"workload": CONFIG_NAMES[config], "tolerance": tol,
-                          "step": f"{s} HPR iterations of the reference's run_inner "
+                  config=wcfg,
+                  run={"step": f"{s} HPR iterations of the reference's run_inner "
                                   "(hprlp from baseline/_ref, its own scipy/numpy path)",
                           "setup_untimed_s": {"scale_problem": t_scale,
                                               "power_method": t_power,
@@ -528,14 +564,16 @@ def run_reference(args):
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
+    dt = 0.0
     for _ in range(args.steps):
+        host_flush()
+        t0 = time.perf_counter()
         step()
-    dt = time.perf_counter() - t0
+        dt += time.perf_counter() - t0
     val = interval * args.steps / dt
     emit(dict(base, value=val, unit="it/s", ms_per_step=1e3 * dt / args.steps,
-              config={"workload": CONFIG_NAMES[config], "tolerance": tol,
-                      "step": f"{interval} HPR iterations (oracle port; baseline/_ref absent)"},
+              config=wcfg,
+              run={"step": f"{interval} HPR iterations (oracle port; baseline/_ref absent)"},
               cpu_baseline={"unit": "it/s", "cores": threads, "kind": "port",
                             "sample": f"{args.steps} x {interval} iterations"}))
 
@@ -672,18 +710,16 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[config], "tolerance": tol, "m": m, "n": n,
-                       "nnz": nnz,
-                       "step": "one full solve to tolerance from HBM-resident input "
+            "config": shared_config(config, tol, m, n, nnz) if ws == 1 else dict(
+                shared_config(config, tol, m, n, nnz), parallelism=f"replicas x{ws}"),
+            "run": {"step": "one full solve to tolerance from HBM-resident input "
                                "(transpose/layout analysis, scaling, power method, "
                                "iterations, checkpoints)",
                        "e2e_step": "solve(problem) on host arrays: pinned H2D upload, setup, "
                                    "solve, D2H of x, y, z",
                        "e2e_steps": e2e_steps,
                        "status": r0.status.value, "iterations_per_solve": r0.iterations,
-                       "wall_time_to_tol_s": t_max / args.steps,
-                       "l2": "256 MB buffer written between timed steps (flush)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+                       "wall_time_to_tol_s": t_max / args.steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": args.traffic if args.traffic is not None
@@ -764,11 +800,10 @@ def run_c5(args, dist, ws, rank, local):
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES["c5"], "tolerance": 1e-8,
-                       "lps_per_rank": hi - lo, "lps_total": C5_COUNT,
-                       "step": "the rank's shard solved to 1e-8 in one launch (one LP per CTA)",
-                       "status": st, "l2": "inputs re-read from HBM each step (490 MB > L2)",
-                       "parallelism": f"batch sharded x{ws}" if ws > 1 else "single GPU"},
+            "config": c5_config(ws),
+            "run": {"lps_per_rank": hi - lo,
+                    "step": "the rank's shard solved to 1e-8 in one launch (one LP per CTA)",
+                    "status": st},
             "roofline": smem_roofline(probs, value),
             "cpu_baseline": cpu,
             "e2e": {"value": its_e2e / t_e2e, "unit": "LP-it/s",
@@ -950,16 +985,14 @@ def run_c4(args, dist, ws, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES["c4"], "m": m, "n": C4_N,
-                       "nnz": m * C4_PER_ROW, "rows_per_rank": rows,
+            "config": c4_config(ws, rows),
+            "run": {"m": m, "nnz": m * C4_PER_ROW,
                        "step": "150 HPR iterations + checkpoint (row-block, NCCL RS/AG per iteration)",
                        "job_iterations_per_sec": its / t_max,
                        "unit_note": "rank-it/s = job iterations/s x ranks (each job iteration "
                                     "advances every rank's 1.25M-row block once)",
                        "one_rank": one_rank, "nccl": comm,
-                       "lambda": lam, "power_iterations": est.iterations,
-                       "l2": "working set > L2 (no flush needed)",
-                       "parallelism": f"row-block x{ws} (NCCL)"},
+                       "lambda": lam, "power_iterations": est.iterations},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": load_traffic("c4") if args.c4_rows == 1_250_000 else None,
