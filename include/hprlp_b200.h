@@ -202,6 +202,8 @@ typedef struct hpr_layout_info_t {
   int64_t bounds_uniform; /* after hpr_scale: bit 0 every scaled lower bound equal, bit 1
                              every upper bound equal (passed as scalars, not streamed) */
   int64_t ts_a, ts_at;   /* blocks of the bulk-copy-streamed (TS) iteration engine (0: off) */
+  int64_t ts_words_a, ts_words_at; /* the TS engine's column-index words (one per entry in
+                             lane-affine / lane-uniform slices; 0: it reads the slot indices) */
 } hpr_layout_info_t;
 int hpr_layout_info(hpr_ctx *ctx, hpr_layout_info_t *info);
 

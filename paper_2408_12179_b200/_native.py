@@ -74,7 +74,8 @@ class HprLayoutInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in ("slices_a", "slices_at", "slots_a", "slots_at",
                                                "long_rows_a", "long_rows_at", "cb_a", "cb_at",
                                                "split_a", "stg_a", "stg_at", "rao_a", "rao_at",
-                                               "bounds_uniform", "ts_a", "ts_at")]
+                                               "bounds_uniform", "ts_a", "ts_at", "ts_words_a",
+                                               "ts_words_at")]
 
 
 class HprBatchProblem(ctypes.Structure):

@@ -73,6 +73,12 @@ int fail(int code, const std::string &msg) {
 #ifndef HPR_X_IMPLICIT
 #define HPR_X_IMPLICIT 1    // HPR inner loop: x re-formed from w inside an interval (EpiXIter)
 #endif
+#ifndef HPR_TS_U_AW
+#define HPR_TS_U_AW 3   // entries per lane per batch of the index-word TS kernel (4: spills)
+#endif
+#ifndef HPR_TS_AW
+#define HPR_TS_AW 0   // 1: TS engine reads per-slice index words (lane-affine / uniform slices: one per entry); C3 x-phase 833 -> 877 us/iteration (slower, profiles/r02_ts_index_words.txt)
+#endif
 #ifndef HPR_COMPACT_HDR
 #define HPR_COMPACT_HDR 1   // compact SELL slices (32 consecutive equal-length rows) skip the per-lane header
 #endif
@@ -404,6 +410,11 @@ struct hpr_ctx {
   long long ts_T[2] = {0, 0};          // block weight targets (0: TS off for A / A^T)
   long long ts_cap_n[2] = {0, 0};      // reserved list entries
   int ts_nb_a = 0, ts_nb_at = 0;
+  // TS index words (SellMat::aw / aptr) of A / A^T, in the layout buffer after
+  // the block lists: reserved at hpr_analyze (ts_aw_cap words, 0: off), filled
+  // at hpr_bind_layout (ts_aw_words used)
+  long long ts_aw_cap[2] = {0, 0}, ts_aw_words[2] = {0, 0};
+  int *ts_aw[2] = {nullptr, nullptr}, *ts_aptr[2] = {nullptr, nullptr};
   // small-LP loop staging (small_smem_plan): cluster size it was planned for,
   // per-CTA slot capacity of A^T / A, dynamic shared-memory bytes
   int small_G = -1, small_cap[2] = {0, 0}, small_smem = 0;
@@ -811,12 +822,59 @@ int ts_select(hpr_ctx *c) {
     // entries: nb + 1 for one range; per column chunk at most one more block
     // and one end entry each (A^T in the row-block overlap path)
     c->ts_cap_n[q] = nb + 1 + (q ? 2LL * kTsMaxChunks : 0);
+    // index words (hpr_tsell.cuh): worst case one word per slot
+    const char *ea = getenv("HPR_TS_AW");
+    c->ts_aw_cap[q] = (ea ? atoi(ea) : HPR_TS_AW) ? S.slots + 16 : 0;
   }
   return HPR_OK;
 }
 
+size_t ts_aw_bytes(const hpr_ctx *c, int q) {
+  const Sell &S = q ? c->sat : c->sa;
+  if (c->ts_T[q] <= 0 || c->ts_aw_cap[q] <= 0) return 0;
+  return align_up(sizeof(int) * (size_t)(S.nslices + 16), 256) +
+         align_up(sizeof(int) * (size_t)c->ts_aw_cap[q], 256);
+}
+
 size_t ts_bytes(const hpr_ctx *c) {
-  return align_up(sizeof(int) * (size_t)(c->ts_cap_n[0] + c->ts_cap_n[1]) + 16, 256);
+  return align_up(sizeof(int) * (size_t)(c->ts_cap_n[0] + c->ts_cap_n[1]) + 16, 256) +
+         ts_aw_bytes(c, 0) + ts_aw_bytes(c, 1);
+}
+
+// Fill the TS index words of A (q = 0) / A^T (q = 1) from the laid-out SELL
+// column indices: per slice, one word per entry when every entry's 32 lane
+// columns are lane-affine or lane-uniform, else the slot words unchanged.
+int ts_aw_layout(hpr_ctx *c, char *base) {
+  cudaStream_t s = c->stream;
+  char *p = base + align_up(sizeof(int) * (size_t)(c->ts_cap_n[0] + c->ts_cap_n[1]) + 16, 256);
+  for (int q = 0; q < 2; ++q) {
+    c->ts_aw[q] = c->ts_aptr[q] = nullptr;
+    c->ts_aw_words[q] = 0;
+    if (ts_aw_bytes(c, q) == 0) continue;
+    const Sell &S = q ? c->sat : c->sa;
+    int *aptr = (int *)p;
+    p += align_up(sizeof(int) * (size_t)(S.nslices + 16), 256);
+    int *aw = (int *)p;
+    p += align_up(sizeof(int) * (size_t)c->ts_aw_cap[q], 256);
+    CK(cudaMemsetAsync(aptr, 0, sizeof(int) * (size_t)(S.nslices + 16), s));
+    const long long thr = 32LL * (S.nslices + 1);
+    k_aw_count<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(S.slice_ptr, S.ci, S.nslices, aptr);
+    CKL();
+    size_t tb = c->L.cub_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(c->ws + c->L.cub_tmp, tb, aptr, aptr, S.nslices + 1, s));
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, aptr + S.nslices, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (total + 16 > c->ts_aw_cap[q]) return fail(HPR_EINVAL, "TS index words exceed their reservation");
+    CK(cudaMemsetAsync(aw, 0, sizeof(int) * (size_t)(total + 16), s));
+    k_aw_fill<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(S.slice_ptr, S.ci, S.nslices, aptr, aw);
+    CKL();
+    c->launches += 3;
+    c->ts_aw[q] = aw;
+    c->ts_aptr[q] = aptr;
+    c->ts_aw_words[q] = total;
+  }
+  return HPR_OK;
 }
 
 int ts_plan(hpr_ctx *c) {
@@ -899,11 +957,23 @@ EpiXIter ts_ef(EpiXIter e) {
 }
 
 template <class Epi>
-int launch_ts(hpr_ctx *c, const SellMat &M, const int *blk, int nblk, const double *xg,
+int launch_ts(hpr_ctx *c, const SellMat &M0, const int *blk, int nblk, const double *xg,
               const Epi &epi) {
-  if (int e = ensure_dyn_smem(k_tsell<HPR_TS_U, Epi>, kTsSmem)) return e;
-  k_tsell<HPR_TS_U, Epi><<<c->num_sms * kTsCps, kTsThreads, kTsSmem, c->stream>>>(M, xg, epi, blk,
-                                                                                  nblk);
+  SellMat M = M0;   // the matrix's index words, when laid out
+  for (int q = 0; q < 2; ++q)
+    if (c->ts_aw[q] && M.slice_ptr == (q ? c->sat : c->sa).slice_ptr) {
+      M.aw = c->ts_aw[q];
+      M.aptr = c->ts_aptr[q];
+    }
+  if (M.aw) {
+    if (int e = ensure_dyn_smem(k_tsell<HPR_TS_U_AW, Epi, true>, kTsSmem)) return e;
+    k_tsell<HPR_TS_U_AW, Epi, true><<<c->num_sms * kTsCps, kTsThreads, kTsSmem, c->stream>>>(
+        M, xg, epi, blk, nblk);
+  } else {
+    if (int e = ensure_dyn_smem(k_tsell<HPR_TS_U, Epi, false>, kTsSmem)) return e;
+    k_tsell<HPR_TS_U, Epi, false><<<c->num_sms * kTsCps, kTsThreads, kTsSmem, c->stream>>>(
+        M, xg, epi, blk, nblk);
+  }
   CKL();
   c->launches += 1;
   return HPR_OK;
@@ -1594,6 +1664,8 @@ int hpr_bind_layout(hpr_ctx *c, void *layout, size_t bytes) {
   if (rc) return rc;
   rc = stg_layout(c, p, c->stat, B.at_rp, B.at_ci, (int)c->d.n);
   if (rc) return rc;
+  rc = ts_aw_layout(c, (char *)c->ts_blk);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(c->stream));
   // the captured graphs hold the layout's pointers and the plans' counts: keep
   // them when a re-analysed problem reproduces both (a re-solve of the same
@@ -2176,6 +2248,8 @@ int hpr_layout_info(hpr_ctx *c, hpr_layout_info_t *info) {
   info->bounds_uniform = c->bounds_uniform;
   info->ts_a = c->ts_a ? c->ts_nb_a : 0;
   info->ts_at = c->ts_at ? c->ts_nb_at : 0;
+  info->ts_words_a = c->ts_aw[0] ? c->ts_aw_words[0] : 0;
+  info->ts_words_at = c->ts_aw[1] ? c->ts_aw_words[1] : 0;
   return HPR_OK;
 }
 

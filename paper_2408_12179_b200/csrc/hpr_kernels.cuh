@@ -154,6 +154,13 @@ struct SellMat {
   // (slice_row / slice_len, 6 bytes a row) is never read -- the row follows
   // from s and the lane, the length from slice_ptr
   int compact;
+  // TS engine only (hpr_tsell.cuh): the slot column indices re-encoded per
+  // slice -- one word per entry where the 32 lanes' columns are lane-affine
+  // (ci = base + lane) or lane-uniform (ci = base, bit 31 set), else the
+  // slice's 32 words per entry unchanged; slice s's words start at aptr[s].
+  // nullptr: the TS engine reads ci
+  const int *aw = nullptr;
+  const int *aptr = nullptr;
 };
 
 constexpr int kSlice = 32;

@@ -52,10 +52,13 @@ constexpr int kTsStages = HPR_TS_STAGES;
 constexpr int kTsSw = HPR_TS_SW;
 constexpr int kTsMaxSl = kTsCap / kTsSw + 1;          // slices per block (plan: weight cut)
 constexpr int kTsPtrInts = (kTsMaxSl + 1 + 8 + 3) & ~3;   // slice offsets, 16-byte aligned superset
-// stage layout: val[cap] f64 | ci[cap] i32 | sptr[kTsPtrInts] i32 | srow[32 maxsl] i32 | slen[32 maxsl] u16
+// stage layout: val[cap] f64 | ci[cap + 8] i32 (slot indices, or the block's
+// index words, 16-byte aligned superset) | sptr[kTsPtrInts] i32 | aptr[kTsPtrInts] i32
+// | srow[32 maxsl] i32 | slen[32 maxsl] u16
 constexpr int kTsOffCi = kTsCap * 8;
-constexpr int kTsOffPtr = kTsOffCi + kTsCap * 4;
-constexpr int kTsOffRow = kTsOffPtr + kTsPtrInts * 4;
+constexpr int kTsOffPtr = kTsOffCi + (kTsCap + 8) * 4;
+constexpr int kTsOffAp = kTsOffPtr + kTsPtrInts * 4;
+constexpr int kTsOffRow = kTsOffAp + kTsPtrInts * 4;
 constexpr int kTsOffLen = kTsOffRow + kTsMaxSl * kSlice * 4;
 constexpr int kTsStageBytes = (kTsOffLen + kTsMaxSl * kSlice * 2 + 127) & ~127;
 constexpr int kTsSmem = kTsStages * kTsStageBytes;
@@ -82,13 +85,60 @@ __global__ void k_ts_plan(const int *slice_ptr, int s_lo, int s_hi, long long T,
   blk[b] = a;
 }
 
+// Index words of the TS engine (SellMat::aw / aptr).  k_aw_count: one warp per
+// slice; cnt[s] = entries per lane when every entry's 32 lane columns are
+// lane-affine (c = c0 + lane) or lane-uniform (c = c0), else 32 x entries
+// (cnt[nslices] = 0; the exclusive scan of cnt is aptr).
+__global__ void k_aw_count(const int *__restrict__ slice_ptr, const int *__restrict__ ci,
+                           int nslices, int *cnt) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw > nslices) return;
+  if (gw == nslices) {
+    if (lane == 0) cnt[nslices] = 0;
+    return;
+  }
+  const int p = slice_ptr[gw], len = (slice_ptr[gw + 1] - p) / kSlice;
+  bool ok = true;
+  for (int k = 0; k < len && ok; ++k) {
+    const int col = ci[p + k * kSlice + lane];
+    const int c0 = __shfl_sync(0xffffffffu, col, 0);
+    const bool aff = __all_sync(0xffffffffu, col == c0 + lane);
+    const bool uni = __all_sync(0xffffffffu, col == c0);
+    ok = aff || uni;
+  }
+  if (lane == 0) cnt[gw] = ok ? len : kSlice * len;
+}
+
+// k_aw_fill: the words -- per entry c0 (lane-affine) or c0 | 2^31 (uniform) for
+// a compressed slice, the slot indices unchanged otherwise
+__global__ void k_aw_fill(const int *__restrict__ slice_ptr, const int *__restrict__ ci,
+                          int nslices, const int *__restrict__ aptr, int *aw) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= nslices) return;
+  const int p = slice_ptr[gw], len = (slice_ptr[gw + 1] - p) / kSlice;
+  const int o = aptr[gw];
+  const bool per_lane = aptr[gw + 1] - o != len;
+  for (int k = 0; k < len; ++k) {
+    const int col = ci[p + k * kSlice + lane];
+    if (per_lane) {
+      aw[o + k * kSlice + lane] = col;
+    } else {
+      const int c0 = __shfl_sync(0xffffffffu, col, 0);
+      const bool uni = __all_sync(0xffffffffu, col == c0);
+      if (lane == 0) aw[o + k] = uni ? (int)((unsigned)c0 | 0x80000000u) : c0;
+    }
+  }
+}
+
 #ifndef HPR_TS_REV
 #define HPR_TS_REV 0         // 1: each CTA walks its blocks last to first (C3: 836.3 vs 833.1 us, off)
 #endif
 // the i-th block a CTA processes, as an index into its round-robin share
 __device__ __forceinline__ int ts_bi(int i, int nmine) { return HPR_TS_REV ? nmine - 1 - i : i; }
 
-template <int U, class Epi>
+template <int U, class Epi, bool AW>
 __global__ void __launch_bounds__(kTsThreads, kTsCps)
 k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict__ blk, int nblk) {
   static_assert(Epi::NQ == 0, "TS engine: iteration epilogues only");
@@ -113,18 +163,23 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
     const uint64_t hpol = policy_evict_normal();
     for (int i0 = 0; i0 < nmine; i0 += 32) {
       // 32 blocks' slice ranges at once (one lane each), handed to lane 0
-      int sb = 0, se = 0, pa = 0, pz = 0;
+      int sb = 0, se = 0, pa = 0, pz = 0, wa = 0, wz = 0;
       if (i0 + lane < nmine) {
         const int b = g + ts_bi(i0 + lane, nmine) * G;
         sb = blk[b];
         se = blk[b + 1];
         pa = M.slice_ptr[sb];
         pz = M.slice_ptr[se];
+        if (AW) {
+          wa = M.aptr[sb];
+          wz = M.aptr[se];
+        }
       }
       const int cnt = min(32, nmine - i0);
       for (int j = 0; j < cnt; ++j) {
         const int s_b = __shfl_sync(0xffffffffu, sb, j), s_e = __shfl_sync(0xffffffffu, se, j);
         const int p_a = __shfl_sync(0xffffffffu, pa, j), p_z = __shfl_sync(0xffffffffu, pz, j);
+        const int w_a = __shfl_sync(0xffffffffu, wa, j), w_z = __shfl_sync(0xffffffffu, wz, j);
         if (lane == 0) {
           const int i = i0 + j, st = i % kTsStages;
           if (i >= kTsStages) mbar_wait(&empty[st], (uint32_t)(((i / kTsStages) - 1) & 1));
@@ -133,14 +188,17 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
           const int q0 = s_b & ~3, q1 = (s_e + 1 + 3) & ~3;      // aligned slice-offset range
           const int nh = s_e > M.compact ? s_e - max(s_b, M.compact) : 0;   // non-compact slices
           const int h0 = max(s_b, M.compact);
-          uint32_t bytes = ns * 12u + (uint32_t)(q1 - q0) * 4u;
+          // index words: the aligned superset [w_a & ~3, (w_z + 3) & ~3)
+          const int a0 = w_a & ~3, a1 = (w_z + 3) & ~3;
+          const uint32_t nwb = AW ? (uint32_t)(a1 - a0) * 4u : ns * 4u;
+          uint32_t bytes = ns * 8u + nwb + (uint32_t)(q1 - q0) * 4u * (AW ? 2u : 1u);
           if (nh > 0) bytes += (uint32_t)nh * (kSlice * 6);
           mbar_expect_tx(&full[st], bytes);
-          if (ns) {
-            bulk_g2s(S, M.val + p_a, ns * 8u, &full[st], pol);
-            bulk_g2s(S + kTsOffCi, M.ci + p_a, ns * 4u, &full[st], pol);
-          }
+          if (ns) bulk_g2s(S, M.val + p_a, ns * 8u, &full[st], pol);
+          if (nwb) bulk_g2s(S + kTsOffCi, AW ? M.aw + a0 : M.ci + p_a, nwb, &full[st], pol);
           bulk_g2s(S + kTsOffPtr, M.slice_ptr + q0, (uint32_t)(q1 - q0) * 4u, &full[st], hpol);
+          if (AW)
+            bulk_g2s(S + kTsOffAp, M.aptr + q0, (uint32_t)(q1 - q0) * 4u, &full[st], hpol);
           if (nh > 0) {
             bulk_g2s(S + kTsOffRow + (h0 - s_b) * kSlice * 4, M.slice_row + (size_t)h0 * kSlice,
                      (uint32_t)nh * kSlice * 4u, &full[st], hpol);
@@ -171,13 +229,27 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
     const double *rv = (const double *)S;
     const int *rc = (const int *)(S + kTsOffCi);
     const int *sptr = (const int *)(S + kTsOffPtr) - (s_b & ~3);   // indexed by slice id
+    const int *aptr = (const int *)(S + kTsOffAp) - (s_b & ~3);
     const int *srow = (const int *)(S + kTsOffRow);
     const unsigned short *slen_l = (const unsigned short *)(S + kTsOffLen);
     mbar_wait(&full[st], (uint32_t)((i / kTsStages) & 1));
     const int p0 = sptr[s_b];
+    const int w0 = AW ? aptr[s_b] & ~3 : 0;
     for (int s = s_b + (warp - rot % kTsWarps + kTsWarps) % kTsWarps; s < s_e; s += kTsWarps) {
       const int a = sptr[s] - p0;   // slot offset inside the stage
       const int slen = (sptr[s + 1] - sptr[s]) / kSlice;
+      // column of entry k: per-lane words (slot order) or one word per entry
+      int wo = a;
+      bool per_lane = true;
+      if (AW) {
+        wo = aptr[s] - w0;
+        per_lane = aptr[s + 1] - aptr[s] != slen;
+      }
+      auto col = [&](int k) -> int {
+        if (per_lane) return rc[wo + k * kSlice + lane];
+        const int wd = rc[wo + k];
+        return (wd & 0x7fffffff) + (wd < 0 ? 0 : lane);
+      };
       int row, len;
       if (s < M.compact) {
         row = s * kSlice + lane;
@@ -197,7 +269,7 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
         if (u < len) {
           const int p = a + u * kSlice + lane;
           v0[u] = rv[p];
-          x0[u] = gather<false>(xg + rc[p]);
+          x0[u] = gather<false>(xg + col(u));
         }
       for (int k = 0; k < slen; k += U) {
         double v1[U], x1[U];
@@ -206,7 +278,7 @@ k_tsell(SellMat M, const double *__restrict__ xg, Epi epi, const int *__restrict
           if (k + U + u < len) {
             const int p = a + (k + U + u) * kSlice + lane;
             v1[u] = rv[p];
-            x1[u] = gather<false>(xg + rc[p]);
+            x1[u] = gather<false>(xg + col(k + U + u));
           }
 #pragma unroll
         for (int u = 0; u < U; ++u)

@@ -501,16 +501,26 @@ def test_flow_lp_downscaled_vs_oracle():
     assert_report_parity(rep, ref, "flow_lp_downscaled")
 
 
-@pytest.mark.parametrize("ts", ["0", "1"])
+@pytest.mark.parametrize("ts", ["0", "1", "1-slot-indices"])
 def test_flow_lp_compact_many_blocks_bit_exact(ts, monkeypatch):
     """A flow LP large enough that every TS CTA walks many blocks of compact
     A^T slices (2 M columns, ~14 blocks per CTA): the cross-block look-ahead of
-    the row operands and the per-block ring phases, bit-exact vs the oracle."""
-    monkeypatch.setenv("HPR_TS", ts)
+    the row operands and the per-block ring phases, bit-exact vs the oracle.
+    Its A^T slices (one arc's 32 commodities) have lane-affine / lane-uniform
+    columns, so the TS engine reads one index word per entry instead of 32
+    (HPR_TS_AW=0: the slot indices, as before)."""
+    monkeypatch.setenv("HPR_TS", ts[0])
+    monkeypatch.setenv("HPR_TS_AW", "0" if ts.endswith("indices") else "1")
     prob = P.generate_flow_lp(5, nodes=1 << 14, out_degree=4, commodities=32)
     dev = _dev(prob)
     info = dev.layout_info()
-    assert (info["ts_a"] > 0 and info["ts_at"] > 0) == (ts == "1")
+    assert (info["ts_a"] > 0 and info["ts_at"] > 0) == (ts[0] == "1")
+    if ts == "1":
+        # every arc slice compressed; the K bypass columns' slice keeps its 32 words per entry
+        assert 0 < info["ts_words_at"] <= info["slots_at"] // 32 + 32 * 3
+        assert 0 < info["ts_words_a"] < info["slots_a"]
+    else:
+        assert info["ts_words_at"] == info["ts_words_a"] == 0
     lam = dev.power(1e-4, 5000).raw * 1.001
     slp = _oracle_on_device_scaling(dev, prob)
     st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 1.0, lam)
