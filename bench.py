@@ -998,6 +998,9 @@ def run_c4(args, dist, ws, rank, local):
                          "traffic": load_traffic("c4") if args.c4_rows == 1_250_000 else None,
                          "kernel": "per-rank iteration (A_g^T partial + slice x-phase + A_g y-phase + collectives)",
                          "bytes_per_iteration": bi_rank, "peak_source": peak_kind},
+            # what binds the rank: one random fp64 operand gather per entry and phase
+            # (y_g from L2 in the A_g^T partial, w's L2-resident column blocks in the y-phase)
+            "roofline_gather": gather_roofline(nnz_rank, its, inner_s),
             "cpu_baseline": c4_cpu_sample(block, m, m1) if ws == 1 and not args.no_cpu else None,
             "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * (2 * C4_N + rows),
