@@ -397,9 +397,12 @@ def test_c1_vs_reference(golden_reports):
 
 
 def test_c2_engines_bit_identical(monkeypatch):
-    """C2: the staged engine (auto-selected for the x-phase) and SELL give the same bits."""
+    """C2: the staged engine (auto-selected for the x-phase) and SELL each give
+    the oracle's bits over 40 fused iterations (oracle C kernels on the
+    device's scaled problem, same lambda)."""
     prob, _ = P.generate_known_solution_lp(2, 50_000, 50_000, 200_000, 2.5e-4)
     out = {}
+    ref = None
     for stg in ("0", None):
         if stg is None:
             monkeypatch.delenv("HPR_STG", raising=False)
@@ -409,11 +412,21 @@ def test_c2_engines_bit_identical(monkeypatch):
         info = dev.layout_info()
         assert (info["stg_a"], info["stg_at"]) == ((0, 0) if stg == "0" else (0, 13))
         lam = dev.power(1e-4, 5000).raw * 1.001
+        if ref is None:
+            slp = _oracle_on_device_scaling(dev, prob)
+            st = O.State(np.zeros(slp.m), np.zeros(slp.n), np.zeros(slp.m), np.zeros(slp.n), 0.9,
+                         lam)
+            for _ in range(40):
+                O.iterate_once(st, slp)
+            ref = (st.y.copy(), st.x.copy(), lam)
+        assert lam == ref[2]
         dev.state_reset()
         dev.run_inner(40, 0, 0, 0.9, lam * 0.9, 2)
         out[stg] = (dev.to_host("y"), dev.to_host("x"))
         dev.close()
-    assert np.array_equal(out["0"][0], out[None][0]) and np.array_equal(out["0"][1], out[None][1])
+    for stg in ("0", None):
+        assert np.array_equal(out[stg][0], ref[0]), stg
+        assert np.array_equal(out[stg][1], ref[1]), stg
 
 
 def test_c2_vs_reference(golden_reports):
