@@ -333,6 +333,44 @@ def cpu_baseline_sample(prob, iters=300):
                       f"sequential per-row sums, OpenMP {threads} threads), setup excluded"}
 
 
+def reference_cpu_sample(prob, scaled, lam, budget_s=10.0):
+    """The reference's own iteration (``hprlp.core.run_inner`` from
+    baseline/_ref: scipy csr_matvec + numpy, one host core) on the same
+    instance in the same run: the problem as this run's GPU scaling left it
+    (bit-identical to the reference's scale_problem, tests/test_gpu_parity.py)
+    and this run's lambda, so the reference's 80-second setup is skipped; two
+    warm-up iterations (the first builds the lazy transpose), then about
+    ``budget_s`` of iterations timed.  None without baseline/_ref."""
+    hprlp = import_reference()
+    if hprlp is None:
+        return None
+    from hprlp.core import ProblemData, SolverState, Variant as RefVariant, run_inner
+    from hprlp.sparse import SparseMatrix as RefSparse
+    ae, ai = prob.a_eq, prob.a_ineq
+    rp = np.concatenate([np.asarray(ae.row_offsets, np.int64),
+                         np.asarray(ai.row_offsets, np.int64)[1:] + int(ae.row_offsets[-1])])
+    ci = np.concatenate([np.asarray(ae.col_indices, np.int64), np.asarray(ai.col_indices, np.int64)])
+    n = int(np.asarray(prob.c).size)
+    a = RefSparse(rp, ci, np.asarray(scaled["a_val_s"], np.float64), int(rp.size - 1), n)
+    data = ProblemData(a=a, b=scaled["b_s"], c=scaled["c_s"], lower=scaled["lower_s"],
+                       upper=scaled["upper_s"], m1=int(ae.nrows))
+    st = SolverState.origin(data, sigma=1.0, lam=float(lam), variant=RefVariant.HPR)
+    run_inner(st, data, 1)                   # builds the lazy transpose
+    t0 = time.perf_counter()
+    run_inner(st, data, 1)
+    t1 = time.perf_counter() - t0
+    iters = int(max(2, min(3000, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    run_inner(st, data, iters)
+    dt = time.perf_counter() - t0
+    return {"value": iters / dt, "unit": "it/s", "cores": 1, "kind": "reference",
+            "sample": f"{iters} HPR iterations of hprlp's run_inner (baseline/_ref: scipy "
+                      "csr_matvec + numpy, single-threaded) on the same instance in this run, "
+                      "scaled by this run's GPU scaling (bit-identical to scale_problem) with "
+                      "this run's lambda, after two warm-up iterations; the reference's own setup "
+                      "(scaling + power method, ~80 s at C3) not repeated"}
+
+
 def _c5_worker(i):
     from oracle import hprlp_oracle as O
     lib = O.load_clib()
@@ -345,18 +383,26 @@ def _c5_worker(i):
 
 
 def c5_cpu_sample(count):
-    """``count`` C5 LPs solved by the oracle in a process pool over all cores;
-    LP-iterations per second of wall time."""
+    """``count`` C5 LPs solved to 1e-8 in a process pool over all cores by the
+    reference itself (``hprlp.solve`` from baseline/_ref) or, without it, the
+    oracle; LP-iterations per second of wall time."""
     import multiprocessing as mp
     cores = cpu_threads()
+    hprlp = import_reference()
+    if hprlp is not None:
+        _C5_REF[:] = [to_reference_problem(hprlp, p) for p in c5_problems(0, count)]
+    fn = _ref_c5_worker if hprlp is not None else _c5_worker
+    who = "hprlp.solve (baseline/_ref)" if hprlp is not None else "the oracle"
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(min(cores, count)) as pool:
-        out = pool.map(_c5_worker, range(count))
+        out = pool.map(fn, range(count))
     dt = time.perf_counter() - t0
+    _C5_REF[:] = []
     its = sum(o[0] for o in out)
-    return {"value": its / dt, "unit": "LP-it/s", "cores": min(cores, count), "kind": "port",
-            "sample": f"{count} of the 4096 C5 LPs solved to 1e-8 by the oracle (one LP per "
+    return {"value": its / dt, "unit": "LP-it/s", "cores": min(cores, count),
+            "kind": "reference" if hprlp is not None else "port",
+            "sample": f"{count} of the 4096 C5 LPs solved to 1e-8 by {who} (one LP per "
                       f"process, {min(cores, count)} processes), wall time incl. setup"}
 
 
@@ -669,6 +715,10 @@ def run_ours(args):
     # diagnostic overwrites the iterate), for the per-kernel roofline
     lay_now = dev.layout_info()
     ph_x_us, ph_y_us = (None, None) if dev.small_path() else dev.time_phases(20)
+    # this run's scaled problem, for the reference's own iteration on the host
+    ref_scaled = None
+    if rank == 0 and ws == 1 and not args.no_cpu and import_reference() is not None:
+        ref_scaled = {k: dev.to_host(k) for k in ("a_val_s", "b_s", "c_s", "lower_s", "upper_s")}
 
     # e2e through the public API from host arrays: every step uploads the
     # problem (pinned staging -> H2D), re-analyses it, solves and copies the
@@ -702,7 +752,12 @@ def run_ours(args):
         lay = r0.device_stats.get("layout", {})
         bu = int(lay.get("bounds_uniform", 0))
         b_req = bi - 8 * n * ((bu & 1) + ((bu >> 1) & 1))
-        cpu = cpu_baseline_sample(prob) if ws == 1 and not args.no_cpu else None
+        port = cpu_baseline_sample(prob) if ws == 1 and not args.no_cpu else None
+        cpu = (reference_cpu_sample(prob, ref_scaled, r0.lambda_estimate)
+               if ref_scaled is not None else None)
+        ref_scaled = None
+        if cpu is None:
+            cpu, port = port, None
         if cpu is not None:
             cpu["host"] = host_info()
         line = {
@@ -737,6 +792,8 @@ def run_ours(args):
             # (phases on the staged engine gather from shared memory instead)
             "roofline_gather": gather_roofline(nnz, its_total, iter_s_total, lay),
             "cpu_baseline": cpu,
+            # the oracle's C kernels on every host thread (test infrastructure), for scale
+            "cpu_baseline_port": port,
             "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -793,7 +850,7 @@ def run_c5(args, dist, ws, rank, local):
     t_e2e, its_e2e = _max_sum(dist, local, e2e_t, e2e_its)
     line = None
     if rank == 0:
-        cpu = c5_cpu_sample(max(cpu_threads(), 16)) if ws == 1 and not args.no_cpu else None
+        cpu = c5_cpu_sample(4 * max(cpu_threads(), 16)) if ws == 1 and not args.no_cpu else None
         line = {
             "metric": "hpr_lp_iterations_per_sec", "value": value, "unit": "LP-it/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
