@@ -34,6 +34,7 @@ namespace hpr {
 // xb_out / zb_out and the candidate slot, x is left alone.
 struct EpiExactX {
   static constexpr int NQ = 0;
+  static constexpr int kMinBlocks = HPR_SELL_MINB_RED;   // 72 registers spill here
   const double *c, *lo, *up, *anc;
   double *x, *u;
   double *xb_out, *zb_out, *cx_out, *cz_out;

@@ -497,13 +497,24 @@ __device__ __forceinline__ void halpern_weights(long long t, double &wa, double 
 // slice 8*window + w), then the long rows are strided over all warps.  Static
 // assignment keeps the per-CTA partial sums deterministic.
 #ifndef HPR_SELL_MINB
-#define HPR_SELL_MINB 6      // min resident CTAs per SM (register cap 80: C3 1033 -> 946 us/iteration)
+#define HPR_SELL_MINB 7      // min resident CTAs per SM of the reduction-free instances (register cap 72; 6 / cap 80: C3 1033 -> 946 us/iteration, 7: 832 -> 824, profiles/r02_sell_minb.txt)
 #endif
+#ifndef HPR_SELL_MINB_RED
+#define HPR_SELL_MINB_RED 6  // instances with per-CTA partial sums (checkpoint epilogues: more live values; spill at 72)
+#endif
+// resident-CTA floor of a reduction-free / reduction epilogue; an epilogue
+// with more live values can ask for the lower floor (static kMinBlocks)
+template <class E, class = void>
+struct sell_min_blocks
+    : std::integral_constant<int, (E::NQ > 0 ? HPR_SELL_MINB_RED : HPR_SELL_MINB)> {};
+template <class E>
+struct sell_min_blocks<E, std::void_t<decltype(E::kMinBlocks)>>
+    : std::integral_constant<int, E::kMinBlocks> {};
 #ifndef HPR_SELL_MINB_GA
-#define HPR_SELL_MINB_GA HPR_SELL_MINB   // the gather-ahead (long-row) instances
+#define HPR_SELL_MINB_GA 6   // the gather-ahead (long-row) instances
 #endif
 template <int U, bool GA, class Epi>
-__global__ void __launch_bounds__(kThreads, GA ? HPR_SELL_MINB_GA : HPR_SELL_MINB)
+__global__ void __launch_bounds__(kThreads, GA ? HPR_SELL_MINB_GA : sell_min_blocks<Epi>::value)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll
