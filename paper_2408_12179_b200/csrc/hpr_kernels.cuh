@@ -511,10 +511,16 @@ template <class E>
 struct sell_min_blocks<E, std::void_t<decltype(E::kMinBlocks)>>
     : std::integral_constant<int, E::kMinBlocks> {};
 #ifndef HPR_SELL_MINB_GA
-#define HPR_SELL_MINB_GA 6   // the gather-ahead (long-row) instances
+#define HPR_SELL_MINB_GA 6   // the gather-ahead (long-row) instances (C2's y-phase: 7 is 1 % slower)
 #endif
+template <class E, class = void>
+struct sell_min_blocks_ga : std::integral_constant<int, HPR_SELL_MINB_GA> {};
+template <class E>
+struct sell_min_blocks_ga<E, std::void_t<decltype(E::kMinBlocksGA)>>
+    : std::integral_constant<int, E::kMinBlocksGA> {};
 template <int U, bool GA, class Epi>
-__global__ void __launch_bounds__(kThreads, GA ? HPR_SELL_MINB_GA : sell_min_blocks<Epi>::value)
+__global__ void __launch_bounds__(kThreads, GA ? sell_min_blocks_ga<Epi>::value
+                                                : sell_min_blocks<Epi>::value)
 k_sell(SellMat M, const double *__restrict__ xg, Epi epi, double *part) {
   double acc[Epi::NQ > 0 ? Epi::NQ : 1];
 #pragma unroll
@@ -664,6 +670,7 @@ struct EpiYIter {
 // hands them to the phase's real epilogue (EpiCarryIn).
 struct EpiCarry {
   static constexpr int NQ = 0;
+  static constexpr int kMinBlocksGA = 7;   // C4's column-split blocks: 72 registers, -1 %
   double *psum;
   int first;
   __device__ bool enter() { return true; }
@@ -673,6 +680,7 @@ struct EpiCarry {
 };
 template <class Epi>
 struct EpiCarryIn : Epi {
+  static constexpr int kMinBlocksGA = 7;
   const double *psum;
   __device__ double init(int r) { return psum[r]; }
 };

@@ -47,8 +47,12 @@ struct PtrSet {
 };
 
 // x-phase partial of A_g^T v (row-block mode): out[j] = s
+#ifndef HPR_STORE_MINB
+#define HPR_STORE_MINB 8   // the A_g^T partial: 64 registers, spill-free (C4 rank -0.7 %)
+#endif
 struct EpiStore {
   static constexpr int NQ = 0;
+  static constexpr int kMinBlocks = HPR_STORE_MINB;
   double *out;
   const PowState *S;   // optional gate (power method)
   __device__ bool enter() { return S == nullptr || !S->done; }
